@@ -1,0 +1,155 @@
+/* B200 FSEP framework -- C ABI of the FSEP MoE-layer step (GPU) and of the
+ * array-level planner entry points it uses every step.
+ *
+ * The reference (/root/reference/proj) stops at the planner: its C ABI
+ * (moeplan.h) emits layouts and routing plans as JSON for one trace layer
+ * (mp_plan_layer_json, /root/reference/proj/src/capi.cpp:218-226 ->
+ * commands.cpp:32-100).  A runtime needs the same computation on raw arrays,
+ * once per (layer, step), without JSON; and it needs the GPU layer step that
+ * consumes the result.  These entry points add exactly that, under the same
+ * conventions as moeplan.h (mp_status returns, thread-local mp_last_error,
+ * opaque caller-owned handles, no exceptions across the ABI, plain pointers and
+ * sizes only -- no torch types).
+ *
+ * Layout of the arrays crossing this boundary (all row-major):
+ *   R  [N][E]  uint64  token-slot counts, row i = source device i   (RoutingMatrix, types.hpp:26-52)
+ *   A  [E][N]  uint8   0/1 replica placement                        (ExpertLayout,  types.hpp:63-87)
+ *   S  [N][E][N] uint64 tokens (src, expert, dst)                   (RoutingPlan,   types.hpp:91-106, dense)
+ *
+ * GPU-side tensors (device pointers unless noted; bf16 = IEEE bfloat16 bits):
+ *   x, y, dy, dx   [T][H] bf16 per rank (virtual mode: the ranks' blocks are concatenated)
+ *   bias           [T][E] fp32 per rank, added to the router logits (routing-skew injection; may be NULL)
+ *   expert weights: w1 (gate) [F][H], w3 (up) [F][H], w2 (down) [H][F] bf16 per expert
+ *   router weight : wg [E][H] bf16
+ * All GPU calls take a cudaStream_t (passed as void*) and are asynchronous
+ * with respect to the host unless stated otherwise.
+ */
+#ifndef MOEPLAN_FSEP_H_
+#define MOEPLAN_FSEP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "moeplan.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ======================= array-level planner ============================== */
+
+typedef struct mp_fsep_planner mp_fsep_planner;
+
+/* A per-layer planner with history, following the runtime's one-iteration lag
+ * (/root/reference/proj/src/sim.cpp:99-149): the layout for step t is
+ * plan_layout(R_0..R_{t-1}) with the layer-salted seed
+ * mix_seed(seed, "layr", layer) (sim.cpp:108-109).  Uses the config's topology,
+ * cost, model.capacity and planner blocks (config.cpp:85-178). */
+mp_status mp_fsep_planner_create(const mp_config* config, uint32_t n_devices, uint32_t layer,
+                                 mp_fsep_planner** out);
+/* Append one observed R (host array, N*E uint64) to the history. */
+mp_status mp_fsep_planner_observe(mp_fsep_planner* planner, const uint64_t* R);
+/* Layout for the next step: plan_layout over the history (planner.cpp:369-414),
+ * or the even-replication layout when the history is empty (sim.cpp:100-103). */
+mp_status mp_fsep_planner_next(mp_fsep_planner* planner, uint8_t* A_out);
+void mp_fsep_planner_free(mp_fsep_planner* planner);
+
+/* One-shot plan_layout on a single R (history = [R]) -- the hot call timed in
+ * the CPU baseline. seed is used as-is (no layer salting). */
+mp_status mp_fsep_plan_layout(uint32_t n_devices, uint32_t n_experts, uint32_t capacity, double bandwidth,
+                              double v_comm, double v_comp, double b_comp, uint32_t epsilon, uint64_t seed,
+                              const uint64_t* R, uint8_t* A_out);
+/* lite_routing (planner.cpp:238-287) on a single-node topology, dense S output. */
+mp_status mp_fsep_lite_routing(uint32_t n_devices, uint32_t n_experts, const uint64_t* R, const uint8_t* A,
+                               uint64_t* S_out);
+/* static_ep_layout (planner.cpp:289-296) / even_replication_layout (:298-307). */
+mp_status mp_fsep_static_layout(uint32_t n_devices, uint32_t n_experts, uint32_t capacity, uint8_t* A_out);
+mp_status mp_fsep_even_layout(uint32_t n_devices, uint32_t n_experts, uint32_t capacity, uint8_t* A_out);
+/* time_cost (cost.cpp:39-73) of lite_routing(R, A) on Topology(1, N, bw, bw). */
+mp_status mp_fsep_time_cost(uint32_t n_devices, uint32_t n_experts, const uint64_t* R, const uint8_t* A,
+                            double bandwidth, double v_comm, double v_comp, double b_comp, double* t_comm,
+                            double* t_comp, double* t_total, uint64_t* max_recv);
+
+/* ========================= GPU FSEP layer step ============================= */
+
+typedef struct mp_fsep_layer mp_fsep_layer;
+
+typedef struct mp_fsep_desc {
+  uint32_t n_experts;     /* E */
+  uint32_t top_k;         /* K */
+  uint32_t hidden;        /* H  (multiple of 256) */
+  uint32_t ffn;           /* F  per-expert SwiGLU width (multiple of 128) */
+  uint32_t max_tokens;    /* T  tokens per rank per step (upper bound) */
+  uint32_t capacity;      /* C  experts materialised per device (K <= C <= E, E <= N*C) */
+  uint32_t world;         /* N  ranks */
+  uint32_t rank;          /* this process's rank (real mode) */
+  uint32_t virtual_ranks; /* 0 = real mode (one process per GPU, N processes);
+                             1 = all N ranks emulated on this GPU (tests/correctness) */
+  uint32_t flags;         /* reserved, 0 */
+  uint64_t max_recv_rows; /* receive-buffer rows per rank; 0 = worst case T*K*N */
+} mp_fsep_desc;
+
+mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_layer** out);
+void mp_fsep_layer_free(mp_fsep_layer* layer);
+
+/* Real multi-GPU mode only.  Exchange protocol (any transport, e.g.
+ * torch.distributed all_gather on the bytes):
+ *   1. every rank: mp_fsep_layer_ipc_handle -> blob of mp_fsep_ipc_bytes() bytes
+ *   2. all-gather the N blobs (rank order); rank 0 also makes an NCCL id with
+ *      mp_fsep_nccl_unique_id and broadcasts it
+ *   3. every rank: mp_fsep_layer_connect(all blobs, nccl id)              */
+size_t mp_fsep_ipc_bytes(void);
+mp_status mp_fsep_nccl_unique_id(void* out, size_t bytes);
+mp_status mp_fsep_layer_ipc_handle(mp_fsep_layer* layer, void* out, size_t bytes);
+mp_status mp_fsep_layer_connect(mp_fsep_layer* layer, const void* all_handles, const void* nccl_id);
+
+/* Parameters.  Weights are given unfused and unsharded (device or pinned host
+ * pointers); each rank keeps its 1/N FSEP shard of every expert.  vrank
+ * selects the emulated rank in virtual mode (ignored in real mode). */
+mp_status mp_fsep_layer_load_expert(mp_fsep_layer* layer, uint32_t expert, const void* w1, const void* w3,
+                                    const void* w2, void* stream);
+mp_status mp_fsep_layer_load_router(mp_fsep_layer* layer, const void* wg, void* stream);
+
+/* Expert layout for the NEXT forward (host array E*N).  The shard restore for
+ * it is issued on the layer's side stream at the next forward. */
+mp_status mp_fsep_layer_set_layout(mp_fsep_layer* layer, const uint8_t* A);
+
+/* Forward / backward of one step.  n_tokens <= max_tokens (per rank). */
+mp_status mp_fsep_layer_forward(mp_fsep_layer* layer, const void* x, const float* bias, uint32_t n_tokens,
+                                void* y, void* stream);
+mp_status mp_fsep_layer_backward(mp_fsep_layer* layer, const void* dy, void* dx, void* stream);
+
+/* R observed by the last forward (host array N*E); synchronises with the
+ * forward's histogram event only (not with the whole step). */
+mp_status mp_fsep_layer_histogram(mp_fsep_layer* layer, uint64_t* R_out);
+
+/* Gradients after backward.  Expert grads are gathered from the fp32 shards
+ * into full unfused fp32 tensors dw1/dw3 [F][H], dw2 [H][F] (device or host
+ * pointers); router grad dwg [E][H] fp32 (sum over this rank's tokens). */
+mp_status mp_fsep_layer_expert_grad(mp_fsep_layer* layer, uint32_t expert, float* dw1, float* dw3, float* dw2,
+                                    void* stream);
+mp_status mp_fsep_layer_router_grad(mp_fsep_layer* layer, uint32_t vrank, float* dwg, void* stream);
+
+/* Test/inspection export of a named internal buffer of rank `vrank` into dst
+ * (device or host).  If dst is NULL only *needed is written.  Names:
+ *   "topk_idx" i32[T][K], "topk_w" f32[T][K], "slot_dst" u32[T][K] (dst<<24|row),
+ *   "R" u64[N][E], "S" u64[N][E][N], "seg_rows" i32[C], "seg_off" i32[C+1],
+ *   "x_rows" bf16[rows][H], "y_rows" bf16[rows][H], "act" bf16[rows][F],
+ *   "h" bf16[rows][2F] (interleaved gate/up 128-col blocks), "restored" bf16[C][3HF],
+ *   "layout" u8[E][N], "status" u32[4] (device error flags)                     */
+mp_status mp_fsep_layer_read(mp_fsep_layer* layer, const char* name, uint32_t vrank, void* dst, uint64_t bytes,
+                             uint64_t* needed);
+
+/* Per-kernel launch count of the last forward+backward, and CUDA-event time of
+ * the dominant kernel class (used by bench.py for the roofline line). */
+mp_status mp_fsep_layer_stats(mp_fsep_layer* layer, uint64_t* kernel_launches, double* gemm_ms, double* gemm_flops);
+
+/* Capture forward+backward into a CUDA graph and replay it (bench path). */
+mp_status mp_fsep_layer_graph_step(mp_fsep_layer* layer, const void* x, const float* bias, uint32_t n_tokens,
+                                   void* y, const void* dy, void* dx, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MOEPLAN_FSEP_H_ */
