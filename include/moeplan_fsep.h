@@ -114,6 +114,14 @@ mp_status mp_fsep_layer_load_router(mp_fsep_layer* layer, const void* wg, void* 
  * it is issued on the layer's side stream at the next forward. */
 mp_status mp_fsep_layer_set_layout(mp_fsep_layer* layer, const uint8_t* A);
 
+/* Attach a planner (mp_fsep_planner_create): after every forward's router the
+ * runtime copies R to pinned host memory on a side stream and runs
+ * observe(R) + next() in a stream host callback, so the layout of step t+1 is
+ * planned from R_t while step t's GEMMs run (one-iteration lag, sim.cpp:114-131),
+ * with no host synchronisation.  NULL detaches.  The planner must outlive the
+ * layer or be detached first. */
+mp_status mp_fsep_layer_attach_planner(mp_fsep_layer* layer, mp_fsep_planner* planner);
+
 /* Forward / backward of one step.  n_tokens <= max_tokens (per rank). */
 mp_status mp_fsep_layer_forward(mp_fsep_layer* layer, const void* x, const float* bias, uint32_t n_tokens,
                                 void* y, void* stream);

@@ -1,0 +1,79 @@
+// Peer-memory data movement for the FSEP layer step over NVLink 5 / NVSwitch:
+// the expert-granular shard restore (unshard) and the cross-rank barrier.
+// Both read the layout and the peer pointer table on the device, so the whole
+// step is enqueued without a host round-trip (and is CUDA-graph capturable).
+#include <cuda_bf16.h>
+
+#include "kernels/fsep_types.cuh"
+#include "kernels/kernels.hpp"
+#include "kernels/routing.hpp"
+
+namespace fsep {
+
+namespace {
+
+// restored[c][p*S : (p+1)*S] = shard_p[e_c][0:S] for every peer p, where e_c is
+// the c-th expert (ascending id) hosted by `rank` under the device layout.
+// FSEP unshard at expert granularity: each device gathers
+// only the C experts it will compute, chunk p from owner p.
+__global__ void __launch_bounds__(256) restore_kernel(const uint8_t* __restrict__ layout, int E, int N, int rank,
+                                                      long long S, long long flat, PeerTable peers,
+                                                      __nv_bfloat16* __restrict__ restored) {
+  __shared__ int s_expert;
+  const int c = blockIdx.y, p = blockIdx.z;
+  if (threadIdx.x == 0) {
+    int seen = -1, found = -1;
+    for (int e = 0; e < E && found < 0; ++e)
+      if (layout[e * N + rank] && ++seen == c) found = e;
+    s_expert = found;
+  }
+  __syncthreads();
+  const int e = s_expert;
+  if (e < 0) return;
+  const uint4* src = reinterpret_cast<const uint4*>(peers.shard[p] + static_cast<long long>(e) * S);
+  uint4* dst = reinterpret_cast<uint4*>(restored + static_cast<long long>(c) * flat + static_cast<long long>(p) * S);
+  const long long n = S / 8;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += static_cast<long long>(gridDim.x) * 256) dst[i] = src[i];
+}
+
+// All-rank barrier: publish `epoch` into every peer's slot for this rank, then
+// wait until every rank has published it here.  System-scope release/acquire
+// orders the preceding peer stores of the step.  Bounded spin: on timeout the
+// kernel records the failure in flags[world] and returns (no trap).
+__global__ void peer_barrier_kernel(unsigned int* const* __restrict__ peer_flags, int world, int rank,
+                                    unsigned int epoch) {
+  const int p = threadIdx.x;
+  if (p < world) {
+    unsigned int* slot = peer_flags[p] + rank;
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(slot), "r"(epoch) : "memory");
+    const unsigned int* mine = peer_flags[rank] + p;
+    unsigned int v = 0;
+    long long spins = 0;
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+      if (static_cast<int>(v - epoch) >= 0) break;
+      if (++spins > (1LL << 26)) {  // ~ seconds
+        atomicOr(peer_flags[rank] + world, 1u);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace
+
+void launch_restore(const uint8_t* layout, int E, int N, int rank, int C, long long S, long long flat,
+                    const PeerTable& peers, __nv_bfloat16* restored, int blocks_per_chunk, cudaStream_t st) {
+  restore_kernel<<<dim3(blocks_per_chunk, C, N), 256, 0, st>>>(layout, E, N, rank, S, flat, peers, restored);
+  count_launch();
+}
+
+void launch_peer_barrier(unsigned int* const* peer_flags, int world, int rank, unsigned int epoch, cudaStream_t st) {
+  peer_barrier_kernel<<<1, 32, 0, st>>>(peer_flags, world, rank, epoch);
+  count_launch();
+}
+
+}  // namespace fsep

@@ -1,0 +1,52 @@
+// Device-side data structures shared by the FSEP routing / dispatch / combine
+// kernels and the host runtime.
+//
+// Receive layout on every device (expert-major, the grouped GEMM's A operand):
+//   for each local slot c (hosted experts in ascending expert id):
+//     rows [seg_off[c], seg_off[c] + seg_rows[c]) hold the tokens routed to that
+//     expert, ordered by (source rank asc, token order within the source);
+//     the segment is padded with zero rows up to a multiple of 128.
+// A token-slot (t, k) of source rank i for expert e with rank r among
+// (i, e)'s slots (ascending t) goes to the replica chosen by lite routing's
+// share/remainder split (planner.cpp:277-282): host index h with
+// cum[h] <= r < cum[h+1], row = row_base[h] + (r - cum[h]).
+#pragma once
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+namespace fsep {
+
+constexpr int kMaxRanks = 16;
+constexpr int kMaxExperts = 128;
+constexpr int kBlockTokens = 128;  // router / ranking tile
+
+struct PeerTable {
+  __nv_bfloat16* x_rows[kMaxRanks];
+  __nv_bfloat16* y_rows[kMaxRanks];
+  __nv_bfloat16* dy_rows[kMaxRanks];
+  __nv_bfloat16* dx_rows[kMaxRanks];
+  unsigned long long* R_all[kMaxRanks];  // [N][E] on each rank
+  float* grad_full[kMaxRanks];           // [C][3HF] restored-expert grads on each rank
+  const __nv_bfloat16* shard[kMaxRanks]; // [E][S] FSEP shards on each rank
+  uint64_t row_capacity;                 // rows of every receive buffer
+};
+
+struct PlanTables {
+  // global view (identical on all ranks)
+  int n_hosts[kMaxExperts];
+  int host_dev[kMaxExperts][kMaxRanks];  // ascending device ids
+  int slot_of[kMaxExperts][kMaxRanks];   // local slot of expert e on device d (-1 if not hosted)
+  // this rank as a source
+  long long src_cum[kMaxExperts][kMaxRanks + 1];
+  long long src_row_base[kMaxExperts][kMaxRanks];
+  // this rank as a destination
+  int slot_expert[kMaxExperts];
+  int seg_rows[kMaxExperts];
+  int seg_rows_pad[kMaxExperts];
+  int seg_off[kMaxExperts];
+  int total_rows;
+  int status;  // bit 0: receive-buffer overflow
+};
+
+}  // namespace fsep

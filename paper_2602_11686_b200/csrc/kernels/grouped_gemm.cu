@@ -1,0 +1,97 @@
+// Host launchers for the grouped tcgen05 GEMM (grouped_gemm.cuh) and TMA
+// tensor-map construction (driver entry point fetched through the runtime, so
+// the library does not link libcuda directly).
+#include <cudaTypedefs.h>
+
+#include <atomic>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "kernels/grouped_gemm.cuh"
+#include "kernels/kernels.hpp"
+
+namespace fsep {
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || p == nullptr)
+      throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+void check_encode(CUresult r, const char* what) {
+  if (r != CUDA_SUCCESS) throw std::runtime_error(std::string("cuTensorMapEncodeTiled failed: ") + what);
+}
+}  // namespace
+
+uint64_t launches_issued() { return g_launches.load(); }
+void count_launch(int n) { g_launches += static_cast<uint64_t>(n); }
+
+CUtensorMap make_tmap_2d(const void* base, uint64_t inner, uint64_t outer, uint64_t pitch_elems, uint32_t box_inner,
+                         uint32_t box_outer) {
+  CUtensorMap m{};
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {pitch_elems * 2};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  check_encode(encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+               "2d");
+  return m;
+}
+
+CUtensorMap make_tmap_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t pitch1, uint64_t pitch2,
+                         uint32_t box0, uint32_t box1) {
+  CUtensorMap m{};
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {pitch1 * 2, pitch2 * 2};
+  const cuuint32_t box[3] = {box0, box1, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  check_encode(encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+               "3d");
+  return m;
+}
+
+namespace {
+template <bool AMN, bool BMN, bool GK, int EPI>
+void launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p, int grid, cudaStream_t st) {
+  auto kern = grouped_gemm_kernel<AMN, BMN, GK, EPI>;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::SMEM_BYTES);
+  });
+  kern<<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(a, b, p);
+  count_launch();
+}
+}  // namespace
+
+void launch_grouped_gemm(GemmKind kind, const CUtensorMap& tmA, const CUtensorMap& tmB, const GroupedGemmArgs& a,
+                         int num_sms, cudaStream_t stream) {
+  if (a.num_groups > gemm::MAX_GROUPS) throw std::runtime_error("grouped gemm: too many groups");
+  if (a.N % 32 != 0) throw std::runtime_error("grouped gemm: N must be a multiple of 32");
+  GemmParams p{a.num_groups, a.group_rows, a.group_off, a.M,    a.N,    a.K,   a.out,
+               a.ldo,        a.out_group_stride, a.out2,    a.ldo2, a.aux, a.ld_aux};
+  switch (kind) {
+    case GemmKind::kFwdGateUp: launch_one<false, false, false, kEpiSwigluFwd>(tmA, tmB, p, num_sms, stream); break;
+    case GemmKind::kFwdDown: launch_one<false, false, false, kEpiBf16>(tmA, tmB, p, num_sms, stream); break;
+    case GemmKind::kBwdDownDgrad: launch_one<false, true, false, kEpiSwigluBwd>(tmA, tmB, p, num_sms, stream); break;
+    case GemmKind::kBwdUpDgrad: launch_one<false, true, false, kEpiBf16>(tmA, tmB, p, num_sms, stream); break;
+    case GemmKind::kBwdWgrad: launch_one<true, true, true, kEpiF32>(tmA, tmB, p, num_sms, stream); break;
+  }
+}
+
+}  // namespace fsep

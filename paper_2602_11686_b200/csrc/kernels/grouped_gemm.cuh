@@ -1,0 +1,336 @@
+// Grouped expert GEMM for the FSEP layer step on sm_100a: tcgen05.mma with
+// fp32 accumulators in TMEM, operands staged by TMA (SWIZZLE_128B) through a
+// 4-stage mbarrier ring, warp-specialised and persistent (one CTA per SM).
+//
+//   warp 0      TMA producer (one elected lane)
+//   warp 1      TMEM allocator + MMA issuer (one elected lane)
+//   warps 2..5  epilogue: TMEM -> registers -> fused op -> global
+//
+// Tile 128 x 256 x 64 (UMMA 128x256x16, cta_group::1).  The accumulator is
+// double-buffered in TMEM (2 x 256 of the 512 columns) so the epilogue of tile i
+// overlaps the MMAs of tile i+1.
+//
+// Two grouping modes, both driven by device-side per-group row counts (no host
+// sync -- the routing kernels write them):
+//   M-grouped (kGroupK=false): C_g[rows_g, N] = A[rows of g, K] * B_g[N, K]^T.
+//       A is the dispatched-token buffer (expert-major, each group padded to
+//       128 rows); B_g the restored weights of local expert slot g (3-D map).
+//   K-grouped (kGroupK=true):  C_g[M, N] = A_g[rows_g, M]^T * B_g[rows_g, N]
+//       (weight gradients: the ragged token dimension is the reduction).
+// Operand majorness is a template parameter (K-major or MN-major for A and B),
+// so dgrad/wgrad read activations and weights in place, without transposes.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "kernels/sm100_ptx.cuh"
+
+namespace fsep {
+
+enum Epi : int {
+  kEpiBf16 = 0,       // out[row, n] = bf16(acc)
+  kEpiSwigluFwd = 1,  // acc tile = [gate 128 | up 128] -> h (bf16, 256 cols) and act = silu(g)*u (128 cols)
+  kEpiSwigluBwd = 2,  // acc = dAct tile (256 f cols); reads h, writes dH = [dgate | dup] interleaved
+  kEpiF32 = 3,        // out_g[m, n] = acc (fp32 weight gradient)
+};
+
+struct GemmParams {
+  int num_groups;
+  const int* group_rows;  // [G] padded rows per group (multiple of 128)
+  const int* group_off;   // [G] first row of group g in the row-indexed operands
+  int M, N, K;            // fixed dims (M: K-grouped only; K: M-grouped only)
+  void* out;
+  long long ldo;
+  long long out_group_stride;  // K-grouped: elements between group outputs
+  void* out2;                  // SwigluFwd: act
+  long long ldo2;
+  const void* aux;  // SwigluBwd: h
+  long long ld_aux;
+};
+
+namespace gemm {
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+constexpr int B_BYTES = BN * BK * 2;  // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int MAX_GROUPS = 256;
+constexpr int THREADS = 192;
+constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/ + (MAX_GROUPS + 1) * 4;
+}  // namespace gemm
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+
+template <bool kAMN, bool kBMN, bool kGroupK, int kEpi>
+__global__ void __launch_bounds__(gemm::THREADS, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const GemmParams p) {
+  using namespace gemm;
+  using namespace fsep::ptx;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  int* tile_start = reinterpret_cast<int*>(smem + STAGES * STAGE_BYTES + 256);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int G = p.num_groups;
+  const int nb = (p.N + BN - 1) / BN;
+
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int g = 0; g < G; ++g) {
+      tile_start[g] = acc;
+      const int rows = p.group_rows[g];
+      acc += kGroupK ? (p.M / BM) * nb : ((rows + BM - 1) / BM) * nb;
+    }
+    tile_start[G] = acc;
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total_tiles = tile_start[G];
+
+  // tile -> (group, m block, n block)
+  auto decode = [&](int t, int& g, int& mb, int& nbk) {
+    g = 0;
+    while (tile_start[g + 1] <= t) ++g;
+    const int local = t - tile_start[g];
+    if (kGroupK) {
+      nbk = local % nb;
+      mb = local / nb;
+    } else {
+      const int mbs = (p.group_rows[g] + BM - 1) / BM;
+      mb = local % mbs;
+      nbk = local / mbs;
+    }
+  };
+  auto k_blocks = [&](int g) { return kGroupK ? p.group_rows[g] / BK : p.K / BK; };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (elect_one()) {
+      const uint64_t pol_a = kGroupK ? policy_evict_first() : policy_evict_last();
+      const uint64_t pol_b = kGroupK ? policy_evict_last() : policy_evict_first();
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        int g, mb, nbk;
+        decode(t, g, mb, nbk);
+        const int nk = k_blocks(g);
+        const int row0 = p.group_off[g];
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          uint8_t* sA = smem + s * STAGE_BYTES;
+          uint8_t* sB = sA + A_BYTES;
+          mbar_arrive_expect_tx(&full_bar[s], STAGE_BYTES);
+          if (!kAMN) {  // A[rows, K] K-major: one 64 x 128 box
+            tma_load_2d(sA, &tmA, &full_bar[s], kb * BK, row0 + mb * BM, pol_a);
+          } else {      // A[rows(K), M] MN-major: two 64(M) x 64(K) boxes
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i)
+              tma_load_2d(sA + i * 8192, &tmA, &full_bar[s], mb * BM + i * 64, row0 + kb * BK, pol_a);
+          }
+          if (!kGroupK) {  // per-group weights: 3-D map (inner, outer, group)
+            if (!kBMN) {
+              tma_load_3d(sB, &tmB, &full_bar[s], kb * BK, nbk * BN, g, pol_b);
+            } else {
+#pragma unroll
+              for (int i = 0; i < BN / 64; ++i)
+                tma_load_3d(sB + i * 8192, &tmB, &full_bar[s], nbk * BN + i * 64, kb * BK, g, pol_b);
+            }
+          } else {  // B[rows(K), N] MN-major
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i)
+              tma_load_2d(sB + i * 8192, &tmB, &full_bar[s], nbk * BN + i * 64, row0 + kb * BK, pol_b);
+          }
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN, kAMN, kBMN);
+    int s = 0;
+    uint32_t ph = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+      int g, mb, nbk;
+      decode(t, g, mb, nbk);
+      const int nk = k_blocks(g);
+      const int as = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      mbar_wait(&tempty_bar[as], aph ^ 1);
+      tc_fence_after();
+      const uint32_t tmem_d = tmem_base + as * BN;
+      if (nk == 0) {
+        if (lane == 0) mbar_arrive(&tfull_bar[as]);
+        __syncwarp();
+        continue;
+      }
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&full_bar[s], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(smem + s * STAGE_BYTES);
+          const uint32_t b0 = a0 + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = kAMN ? smem_desc(a0 + k * 2048, 8192, 1024) : smem_desc(a0 + k * 32, 16, 1024);
+            const uint64_t bd = kBMN ? smem_desc(b0 + k * 2048, 8192, 1024) : smem_desc(b0 + k * 32, 16, 1024);
+            umma_bf16(tmem_d, ad, bd, idesc, (kb | k) ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[s]);
+          if (kb == nk - 1) umma_commit(&tfull_bar[as]);
+        }
+        __syncwarp();
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const uint32_t quarter = warp & 3;           // TMEM lane quarter this warp may access
+    const int r = static_cast<int>(quarter * 32 + lane);  // row within the tile
+    int it = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+      int g, mb, nbk;
+      decode(t, g, mb, nbk);
+      const int as = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      mbar_wait(&tfull_bar[as], aph);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + ((quarter * 32) << 16) + as * BN;
+      const bool empty_k = k_blocks(g) == 0;
+      if (kEpi == kEpiF32) {
+        float* out = static_cast<float*>(p.out) + static_cast<long long>(g) * p.out_group_stride +
+                     static_cast<long long>(mb * BM + r) * p.ldo;
+#pragma unroll 1
+        for (int j = 0; j < BN / 32; ++j) {
+          const int col = nbk * BN + j * 32;
+          if (col >= p.N) break;
+          float v[32];
+          if (empty_k) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          } else {
+            tmem_ld32(taddr + j * 32, v);
+          }
+          float4* dst = reinterpret_cast<float4*>(out + col);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+      } else if (kEpi == kEpiBf16) {
+        const long long row = p.group_off[g] + mb * BM + r;
+        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
+#pragma unroll 1
+        for (int j = 0; j < BN / 32; ++j) {
+          const int col = nbk * BN + j * 32;
+          if (col >= p.N) break;
+          float v[32];
+          tmem_ld32(taddr + j * 32, v);
+          uint4* dst = reinterpret_cast<uint4*>(out + col);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dst[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                                pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+        }
+      } else if (kEpi == kEpiSwigluFwd) {
+        // Accumulator columns [0,128) = gate f in [f0, f0+128), [128,256) = up.
+        const long long row = p.group_off[g] + mb * BM + r;
+        __nv_bfloat16* h = static_cast<__nv_bfloat16*>(p.out) + row * p.ldo + nbk * BN;
+        __nv_bfloat16* act = static_cast<__nv_bfloat16*>(p.out2) + row * p.ldo2 + nbk * (BN / 2);
+#pragma unroll 1
+        for (int j = 0; j < 4; ++j) {
+          float gv[32], uv[32];
+          tmem_ld32(taddr + j * 32, gv);
+          tmem_ld32(taddr + 128 + j * 32, uv);
+          uint4* hg = reinterpret_cast<uint4*>(h + j * 32);
+          uint4* hu = reinterpret_cast<uint4*>(h + 128 + j * 32);
+          uint4* ao = reinterpret_cast<uint4*>(act + j * 32);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            hg[i] = make_uint4(pack_bf16(gv[8 * i], gv[8 * i + 1]), pack_bf16(gv[8 * i + 2], gv[8 * i + 3]),
+                               pack_bf16(gv[8 * i + 4], gv[8 * i + 5]), pack_bf16(gv[8 * i + 6], gv[8 * i + 7]));
+            hu[i] = make_uint4(pack_bf16(uv[8 * i], uv[8 * i + 1]), pack_bf16(uv[8 * i + 2], uv[8 * i + 3]),
+                               pack_bf16(uv[8 * i + 4], uv[8 * i + 5]), pack_bf16(uv[8 * i + 6], uv[8 * i + 7]));
+            float a[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) a[q] = silu_f(gv[8 * i + q]) * uv[8 * i + q];
+            ao[i] = make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]),
+                               pack_bf16(a[6], a[7]));
+          }
+        }
+      } else {  // kEpiSwigluBwd
+        const long long row = p.group_off[g] + mb * BM + r;
+        const __nv_bfloat16* h = static_cast<const __nv_bfloat16*>(p.aux) + row * p.ld_aux;
+        __nv_bfloat16* dh = static_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
+#pragma unroll 1
+        for (int j = 0; j < BN / 32; ++j) {
+          const int f = nbk * BN + j * 32;
+          if (f >= p.N) break;
+          const int hcol = (f / 128) * 256 + (f % 128);
+          float da[32];
+          tmem_ld32(taddr + j * 32, da);
+          const uint4* hg4 = reinterpret_cast<const uint4*>(h + hcol);
+          const uint4* hu4 = reinterpret_cast<const uint4*>(h + hcol + 128);
+          uint4* dg4 = reinterpret_cast<uint4*>(dh + hcol);
+          uint4* du4 = reinterpret_cast<uint4*>(dh + hcol + 128);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint4 gq = hg4[i], uq = hu4[i];
+            const __nv_bfloat16* gb = reinterpret_cast<const __nv_bfloat16*>(&gq);
+            const __nv_bfloat16* ub = reinterpret_cast<const __nv_bfloat16*>(&uq);
+            float dg[8], du[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float gg = __bfloat162float(gb[q]);
+              const float uu = __bfloat162float(ub[q]);
+              const float sg = 1.0f / (1.0f + __expf(-gg));
+              const float d = da[8 * i + q];
+              du[q] = d * gg * sg;
+              dg[q] = d * uu * sg * (1.0f + gg * (1.0f - sg));
+            }
+            dg4[i] = make_uint4(pack_bf16(dg[0], dg[1]), pack_bf16(dg[2], dg[3]), pack_bf16(dg[4], dg[5]),
+                                pack_bf16(dg[6], dg[7]));
+            du4[i] = make_uint4(pack_bf16(du[0], du[1]), pack_bf16(du[2], du[3]), pack_bf16(du[4], du[5]),
+                                pack_bf16(du[6], du[7]));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[as]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+}  // namespace fsep

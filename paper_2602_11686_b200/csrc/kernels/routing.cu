@@ -1,0 +1,634 @@
+// Router, ranking, lite-routing assignment, dispatch/combine and their
+// backward passes for the FSEP layer step (sm_100a, CUDA cores; all of these
+// are HBM/NVLink-bound byte movers or tiny integer work).
+//
+// Bit-exactness contract with the CPU oracle (oracle/layer_oracle.py):
+//  * router logits use a canonical fp32 order: lane l of a warp accumulates
+//    x[256c + 8l + j] * wg[e, 256c + 8l + j] over (c, j) in order with FMA
+//    (exact products: both operands are bf16), then a fixed xor butterfly
+//    16,8,4,2,1; the per-token fp32 bias is added last;
+//  * top-k picks the largest logit, ties to the lowest expert id;
+//  * token ranks within (source, expert) follow ascending token index, and the
+//    replica split reproduces lite_routing (planner.cpp:277-282).
+#include <cuda_bf16.h>
+
+#include <cfloat>
+#include <stdexcept>
+
+#include "kernels/fsep_types.cuh"
+#include "kernels/kernels.hpp"
+#include "kernels/routing.hpp"
+
+namespace fsep {
+
+namespace {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& q, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+__device__ __forceinline__ uint4 f32_to_bf16x8(const float (&f)[8]) {
+  uint4 q;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return q;
+}
+
+// ------------------------------------------------------------------ router
+// One block = 128 tokens (4 warps x 32 tokens, one token at a time per warp).
+// Emits top-k ids / gate weights, per-block expert counts and each slot's rank
+// within its block (token order), which the scan turns into global ranks.
+template <int CH>  // H / 256
+__global__ void __launch_bounds__(128) router_kernel(const __nv_bfloat16* __restrict__ x,
+                                                     const __nv_bfloat16* __restrict__ wg,
+                                                     const float* __restrict__ bias, int T, int E, int K,
+                                                     int* __restrict__ topk_idx, float* __restrict__ topk_w,
+                                                     int* __restrict__ intra_rank, int* __restrict__ blk_hist) {
+  constexpr int H = CH * 256;
+  __shared__ int s_idx[kBlockTokens][8];
+  __shared__ unsigned s_mask[kMaxExperts][4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < kMaxExperts * 4; i += blockDim.x) (&s_mask[0][0])[i] = 0u;
+  __syncthreads();
+
+  for (int tt = 0; tt < 32; ++tt) {
+    const int tl = warp * 32 + tt;
+    const int t = blockIdx.x * kBlockTokens + tl;
+    if (t >= T) break;
+    uint4 xv[CH];
+    const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * H);
+#pragma unroll
+    for (int c = 0; c < CH; ++c) xv[c] = __ldg(xr + c * 32 + lane);
+    // expert e's logit ends up in lane e % 32, register slot e / 32
+    float mine[kMaxExperts / 32];
+#pragma unroll
+    for (int q = 0; q < kMaxExperts / 32; ++q) mine[q] = -FLT_MAX;
+#pragma unroll
+    for (int q = 0; q < kMaxExperts / 32; ++q) {
+      for (int ee = 0; ee < 32; ++ee) {
+        const int e = q * 32 + ee;
+        if (e >= E) break;
+        const uint4* wr = reinterpret_cast<const uint4*>(wg + static_cast<size_t>(e) * H);
+        float acc = 0.f;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          float xf[8], wf[8];
+          bf16x8_to_f32(xv[c], xf);
+          bf16x8_to_f32(__ldg(wr + c * 32 + lane), wf);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc = __fmaf_rn(xf[j], wf[j], acc);
+        }
+        acc = warp_sum(acc);  // xor butterfly 16,8,4,2,1 -- identical on all lanes
+        if (bias) acc = __fadd_rn(acc, __ldg(bias + static_cast<size_t>(t) * E + e));
+        if (ee == lane) mine[q] = acc;
+      }
+    }
+    // top-k: warp argmax K times (largest value, lowest id on ties)
+    float sel_v[8];
+    int sel_e[8];
+    for (int k = 0; k < K; ++k) {
+      float bv = -FLT_MAX;
+      int be = 0x7fffffff;
+#pragma unroll
+      for (int q = 0; q < kMaxExperts / 32; ++q) {
+        const int e = q * 32 + lane;
+        if (e < E && (mine[q] > bv || (mine[q] == bv && e < be))) {
+          bv = mine[q];
+          be = e;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+        if (ov > bv || (ov == bv && oe < be)) {
+          bv = ov;
+          be = oe;
+        }
+      }
+      sel_v[k] = bv;
+      sel_e[k] = be;
+#pragma unroll
+      for (int q = 0; q < kMaxExperts / 32; ++q)  // exclude the winner (below -FLT_MAX)
+        if (q == (be >> 5) && (be & 31) == lane) mine[q] = -INFINITY;
+    }
+    if (lane == 0) {
+      float w[8], s = 0.f;
+      for (int k = 0; k < K; ++k) {
+        w[k] = expf(sel_v[k] - sel_v[0]);
+        s += w[k];
+      }
+      for (int k = 0; k < K; ++k) {
+        topk_idx[static_cast<size_t>(t) * K + k] = sel_e[k];
+        topk_w[static_cast<size_t>(t) * K + k] = w[k] / s;
+        s_idx[tl][k] = sel_e[k];
+        atomicOr(&s_mask[sel_e[k]][warp], 1u << tt);
+      }
+    }
+  }
+  __syncthreads();
+  // per-slot rank within the block: tokens with the same expert before me
+  const int tl = threadIdx.x;
+  const int t = blockIdx.x * kBlockTokens + tl;
+  if (t < T) {
+    const int w = tl >> 5, l = tl & 31;
+    for (int k = 0; k < K; ++k) {
+      const int e = s_idx[tl][k];
+      int r = __popc(s_mask[e][w] & ((1u << l) - 1u));
+      for (int ww = 0; ww < w; ++ww) r += __popc(s_mask[e][ww]);
+      intra_rank[static_cast<size_t>(t) * K + k] = r;
+    }
+  }
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    blk_hist[static_cast<size_t>(blockIdx.x) * E + e] =
+        __popc(s_mask[e][0]) + __popc(s_mask[e][1]) + __popc(s_mask[e][2]) + __popc(s_mask[e][3]);
+}
+
+// Exclusive scan of per-block counts per expert -> block bases; R row of this
+// rank is published into every rank's R_all (peer stores; local in N=1).
+__global__ void block_scan_kernel(const int* __restrict__ blk_hist, int nblk, int E, int* __restrict__ blk_base,
+                                  PeerTable peers, int rank, int world) {
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    long long acc = 0;
+    for (int b = 0; b < nblk; ++b) {
+      blk_base[static_cast<size_t>(b) * E + e] = static_cast<int>(acc);
+      acc += blk_hist[static_cast<size_t>(b) * E + e];
+    }
+    for (int p = 0; p < world; ++p) peers.R_all[p][static_cast<size_t>(rank) * E + e] = acc;
+  }
+}
+
+__device__ __forceinline__ long long split_amount(long long tokens, int n, int t) {
+  return tokens / n + (t < tokens % n ? 1 : 0);
+}
+
+// Lite routing on device (planner.cpp:238-287 for a single-node topology) and
+// the receive layout of every device.  One block; E <= 128, N <= 16.
+__global__ void plan_kernel(const unsigned long long* __restrict__ R_all, const uint8_t* __restrict__ layout, int E,
+                            int N, int rank, PlanTables* __restrict__ pt, long long row_capacity) {
+  __shared__ int s_seg_off[kMaxRanks][kMaxExperts];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < E; e += blockDim.x) {
+    int n = 0;
+    for (int d = 0; d < N; ++d)
+      if (layout[e * N + d]) pt->host_dev[e][n++] = d;
+    pt->n_hosts[e] = n;
+  }
+  __syncthreads();
+  // per destination: slots in ascending expert order, padded segment offsets
+  for (int d = tid; d < N; d += blockDim.x) {
+    int c = 0;
+    long long off = 0;
+    for (int e = 0; e < E; ++e) {
+      if (!layout[e * N + d]) {
+        pt->slot_of[e][d] = -1;
+        continue;
+      }
+      const int nh = pt->n_hosts[e];
+      int t = 0;
+      while (pt->host_dev[e][t] != d) ++t;
+      long long rows = 0;
+      for (int i = 0; i < N; ++i) rows += split_amount(static_cast<long long>(R_all[i * E + e]), nh, t);
+      pt->slot_of[e][d] = c;
+      s_seg_off[d][c] = static_cast<int>(off);
+      if (d == rank) {
+        pt->slot_expert[c] = e;
+        pt->seg_rows[c] = static_cast<int>(rows);
+        pt->seg_rows_pad[c] = static_cast<int>((rows + 127) / 128 * 128);
+        pt->seg_off[c] = static_cast<int>(off);
+      }
+      off += (rows + 127) / 128 * 128;
+      ++c;
+    }
+    if (d == rank) {
+      pt->total_rows = static_cast<int>(off);
+      pt->status = off > row_capacity ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  // this rank as a source: per expert, cumulative split and destination rows
+  for (int e = tid; e < E; e += blockDim.x) {
+    const int nh = pt->n_hosts[e];
+    const long long tokens = static_cast<long long>(R_all[rank * E + e]);
+    long long cum = 0;
+    for (int t = 0; t < nh; ++t) {
+      const int d = pt->host_dev[e][t];
+      long long before = 0;  // rows from lower-ranked sources on d for e
+      for (int i = 0; i < rank; ++i) before += split_amount(static_cast<long long>(R_all[i * E + e]), nh, t);
+      pt->src_cum[e][t] = cum;
+      pt->src_row_base[e][t] = s_seg_off[d][pt->slot_of[e][d]] + before;
+      cum += split_amount(tokens, nh, t);
+    }
+    pt->src_cum[e][nh] = cum;
+  }
+}
+
+// Zero the padding rows of this rank's receive buffers (X rows and dY rows) so
+// the GEMMs may run over padded segments and the wgrad reduction stays exact.
+__global__ void zero_pad_kernel(const PlanTables* __restrict__ pt, int C, int H, __nv_bfloat16* x_rows,
+                                __nv_bfloat16* dy_rows) {
+  const int c = blockIdx.y;
+  if (c >= C) return;
+  const int rows = pt->seg_rows[c], pad = pt->seg_rows_pad[c] - rows;
+  const size_t base = static_cast<size_t>(pt->seg_off[c] + rows) * H;
+  const size_t n = static_cast<size_t>(pad) * H / 8;
+  uint4 z = make_uint4(0, 0, 0, 0);
+  for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    reinterpret_cast<uint4*>(x_rows + base)[i] = z;
+    reinterpret_cast<uint4*>(dy_rows + base)[i] = z;
+  }
+}
+
+// ------------------------------------------------------------------ dispatch
+// Warp per token: resolve each slot's (device, row), record it, copy the token
+// row once from HBM and store it K times (local HBM or a peer over NVLink).
+template <int CH>
+__global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int K, int E,
+                                                       const int* __restrict__ topk_idx,
+                                                       const int* __restrict__ intra_rank,
+                                                       const int* __restrict__ blk_base,
+                                                       const PlanTables* __restrict__ pt, PeerTable peers,
+                                                       uint32_t* __restrict__ slot_dst) {
+  constexpr int H = CH * 256;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  uint4* dst_row[8];
+  for (int k = 0; k < K; ++k) {
+    const int e = topk_idx[static_cast<size_t>(t) * K + k];
+    const long long r = blk_base[static_cast<size_t>(t / kBlockTokens) * E + e] + intra_rank[static_cast<size_t>(t) * K + k];
+    int h = 0;
+    while (pt->src_cum[e][h + 1] <= r) ++h;
+    const int d = pt->host_dev[e][h];
+    const long long row = pt->src_row_base[e][h] + (r - pt->src_cum[e][h]);
+    if (lane == 0) slot_dst[static_cast<size_t>(t) * K + k] = (static_cast<uint32_t>(d) << 24) | static_cast<uint32_t>(row);
+    dst_row[k] = (static_cast<uint64_t>(row) < peers.row_capacity)
+                     ? reinterpret_cast<uint4*>(peers.x_rows[d] + static_cast<size_t>(row) * H)
+                     : nullptr;
+  }
+  const uint4* src = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * H);
+  uint4 v[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) v[c] = __ldg(src + c * 32 + lane);
+  for (int k = 0; k < K; ++k) {
+    if (!dst_row[k]) continue;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) dst_row[k][c * 32 + lane] = v[c];
+  }
+}
+
+__device__ __forceinline__ const uint4* row_ptr(__nv_bfloat16* const* bufs, uint32_t code, int H) {
+  return reinterpret_cast<const uint4*>(bufs[code >> 24] + static_cast<size_t>(code & 0xFFFFFFu) * H);
+}
+
+// ------------------------------------------------------------------ combine
+// out[t] = sum_k w[t,k] * y[slot(t,k)]  (fp32 accumulate in k order, bf16 out)
+template <int CH>
+__global__ void __launch_bounds__(256) combine_kernel(int T, int K, const float* __restrict__ topk_w,
+                                                      const uint32_t* __restrict__ slot_dst, PeerTable peers,
+                                                      __nv_bfloat16* __restrict__ out) {
+  constexpr int H = CH * 256;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  uint4* o = reinterpret_cast<uint4*>(out + static_cast<size_t>(t) * H);
+#pragma unroll
+  for (int c0 = 0; c0 < CH; c0 += 4) {
+    float acc[4][8];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[c][j] = 0.f;
+    for (int k = 0; k < K; ++k) {
+      const float w = topk_w[static_cast<size_t>(t) * K + k];
+      const uint4* y = row_ptr(peers.y_rows, slot_dst[static_cast<size_t>(t) * K + k], H);
+      uint4 q[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c0 + c < CH) q[c] = y[(c0 + c) * 32 + lane];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c0 + c >= CH) break;
+        float f[8];
+        bf16x8_to_f32(q[c], f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[c][j] = __fmaf_rn(w, f[j], acc[c][j]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (c0 + c < CH) o[(c0 + c) * 32 + lane] = f32_to_bf16x8(acc[c]);
+  }
+}
+
+// ------------------------------------------------------------- combine bwd
+// dy[slot(t,k)] = w[t,k] * dout[t]   (scattered back to the expert's device)
+// dw[t,k]       = <dout[t], y[slot(t,k)]>
+// dl[t,k]       = w_k (dw_k - sum_j w_j dw_j)       (softmax-over-top-k backward)
+template <int CH>
+__global__ void __launch_bounds__(256) combine_bwd_kernel(int T, int K, const __nv_bfloat16* __restrict__ dout,
+                                                          const float* __restrict__ topk_w,
+                                                          const uint32_t* __restrict__ slot_dst, PeerTable peers,
+                                                          float* __restrict__ dl) {
+  constexpr int H = CH * 256;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const uint4* g = reinterpret_cast<const uint4*>(dout + static_cast<size_t>(t) * H);
+  float dot[8];
+  float w[8];
+  for (int k = 0; k < K; ++k) {
+    dot[k] = 0.f;
+    w[k] = topk_w[static_cast<size_t>(t) * K + k];
+  }
+#pragma unroll
+  for (int c0 = 0; c0 < CH; c0 += 4) {
+    float gf[4][8];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (c0 + c < CH) bf16x8_to_f32(__ldg(g + (c0 + c) * 32 + lane), gf[c]);
+    for (int k = 0; k < K; ++k) {
+      const uint32_t code = slot_dst[static_cast<size_t>(t) * K + k];
+      const uint4* y = row_ptr(peers.y_rows, code, H);
+      uint4* dy = const_cast<uint4*>(row_ptr(peers.dy_rows, code, H));
+      uint4 q[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c0 + c < CH) q[c] = y[(c0 + c) * 32 + lane];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c0 + c >= CH) break;
+        float f[8], s[8];
+        bf16x8_to_f32(q[c], f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          dot[k] = __fmaf_rn(gf[c][j], f[j], dot[k]);
+          s[j] = w[k] * gf[c][j];
+        }
+        dy[(c0 + c) * 32 + lane] = f32_to_bf16x8(s);
+      }
+    }
+  }
+  float dw[8];
+  float mix = 0.f;
+  for (int k = 0; k < K; ++k) {
+    dw[k] = warp_sum(dot[k]);
+    mix += w[k] * dw[k];
+  }
+  if (lane == 0)
+    for (int k = 0; k < K; ++k) dl[static_cast<size_t>(t) * K + k] = w[k] * (dw[k] - mix);
+}
+
+// ----------------------------------------------------------- unpermute bwd
+// dx[t] = sum_k dX_rows[slot(t,k)] + sum_k dl[t,k] * wg[e_k]   (router path)
+template <int CH>
+__global__ void __launch_bounds__(256) unpermute_bwd_kernel(int T, int K, const int* __restrict__ topk_idx,
+                                                            const float* __restrict__ dl,
+                                                            const uint32_t* __restrict__ slot_dst,
+                                                            const __nv_bfloat16* __restrict__ wg, PeerTable peers,
+                                                            __nv_bfloat16* __restrict__ dx) {
+  constexpr int H = CH * 256;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  uint4* o = reinterpret_cast<uint4*>(dx + static_cast<size_t>(t) * H);
+#pragma unroll
+  for (int c0 = 0; c0 < CH; c0 += 4) {
+    float acc[4][8];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[c][j] = 0.f;
+    for (int k = 0; k < K; ++k) {
+      const uint4* r = row_ptr(peers.dx_rows, slot_dst[static_cast<size_t>(t) * K + k], H);
+      const float d = dl[static_cast<size_t>(t) * K + k];
+      const uint4* w = reinterpret_cast<const uint4*>(wg + static_cast<size_t>(topk_idx[static_cast<size_t>(t) * K + k]) * H);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c0 + c >= CH) break;
+        float f[8], wf[8];
+        bf16x8_to_f32(r[(c0 + c) * 32 + lane], f);
+        bf16x8_to_f32(__ldg(w + (c0 + c) * 32 + lane), wf);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[c][j] += f[j] + d * wf[j];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (c0 + c < CH) o[(c0 + c) * 32 + lane] = f32_to_bf16x8(acc[c]);
+  }
+}
+
+// ------------------------------------------------------------ router wgrad
+// partial[split][e][col] = sum over the split's tokens of dl[t,k] * x[t,col]
+// for e = topk_idx[t,k]; reduced over splits in fixed order by the second kernel.
+__global__ void __launch_bounds__(256) router_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ x, int T, int H,
+                                                                   int K, int E, const int* __restrict__ topk_idx,
+                                                                   const float* __restrict__ dl, int tokens_per_split,
+                                                                   float* __restrict__ partial) {
+  extern __shared__ float s_acc[];  // [E][256]
+  const int col = blockIdx.x * 256 + threadIdx.x;
+  for (int e = 0; e < E; ++e) s_acc[e * 256 + threadIdx.x] = 0.f;
+  const int t0 = blockIdx.y * tokens_per_split;
+  const int t1 = min(T, t0 + tokens_per_split);
+  for (int t = t0; t < t1; ++t) {
+    const float xv = __bfloat162float(x[static_cast<size_t>(t) * H + col]);
+    for (int k = 0; k < K; ++k) {
+      const int e = topk_idx[static_cast<size_t>(t) * K + k];
+      s_acc[e * 256 + threadIdx.x] += dl[static_cast<size_t>(t) * K + k] * xv;
+    }
+  }
+  for (int e = 0; e < E; ++e)
+    partial[(static_cast<size_t>(blockIdx.y) * E + e) * H + col] = s_acc[e * 256 + threadIdx.x];
+}
+
+__global__ void router_wgrad_reduce_kernel(const float* __restrict__ partial, int splits, int EH,
+                                           float* __restrict__ dwg) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= EH) return;
+  float s = 0.f;
+  for (int p = 0; p < splits; ++p) s += partial[static_cast<size_t>(p) * EH + i];
+  dwg[i] = s;
+}
+
+// ------------------------------------------------------------ grad RS
+// Owner `rank` sums chunk `rank` of every expert's gradient over the devices
+// that hosted a replica this step (ascending device order -> deterministic),
+// reading the replicas' fp32 gradients in place (peer loads over NVLink).
+__global__ void grad_reduce_scatter_kernel(const PlanTables* __restrict__ pt, PeerTable peers, int E, int rank,
+                                           long long S, long long flat, float* __restrict__ grad_shard) {
+  const int e = blockIdx.y;
+  const int nh = pt->n_hosts[e];
+  const float4* src[kMaxRanks];
+  for (int h = 0; h < nh; ++h) {
+    const int d = pt->host_dev[e][h];
+    src[h] = reinterpret_cast<const float4*>(peers.grad_full[d] + static_cast<long long>(pt->slot_of[e][d]) * flat +
+                                             static_cast<long long>(rank) * S);
+  }
+  float4* dst = reinterpret_cast<float4*>(grad_shard + static_cast<long long>(e) * S);
+  for (long long i = blockIdx.x * blockDim.x + threadIdx.x; i < S / 4; i += gridDim.x * blockDim.x) {
+    float4 a = src[0][i];
+    for (int h = 1; h < nh; ++h) {
+      const float4 b = src[h][i];
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+    }
+    dst[i] = a;
+  }
+}
+
+// ------------------------------------------------------------ weight packing
+// flat[3HF] = [W13 interleaved: rows 256b+q (q<128) = w1[128b+q], 256b+128+q = w3[128b+q]; W2]
+__global__ void pack_expert_kernel(const __nv_bfloat16* __restrict__ w1, const __nv_bfloat16* __restrict__ w3,
+                                   const __nv_bfloat16* __restrict__ w2, int H, int F,
+                                   __nv_bfloat16* __restrict__ flat) {
+  const long long n13 = 2LL * F * H, total = 3LL * F * H;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < total; i += static_cast<long long>(gridDim.x) * 256) {
+    if (i < n13) {
+      const long long row = i / H, col = i % H;
+      const long long b = row / 256, q = row % 256;
+      const long long src_row = b * 128 + (q % 128);
+      flat[i] = (q < 128 ? w1 : w3)[src_row * H + col];
+    } else {
+      flat[i] = w2[i - n13];
+    }
+  }
+}
+
+// Inverse of pack_expert for fp32 gradients, restricted to [lo, hi) of the flat
+// vector (a rank's shard chunk); elements outside are not written.
+__global__ void unpack_grad_kernel(const float* __restrict__ chunk, long long lo, long long hi, int H, int F,
+                                   float* __restrict__ dw1, float* __restrict__ dw3, float* __restrict__ dw2) {
+  const long long n13 = 2LL * F * H;
+  for (long long i = lo + blockIdx.x * 256LL + threadIdx.x; i < hi; i += static_cast<long long>(gridDim.x) * 256) {
+    const float v = chunk[i - lo];
+    if (i < n13) {
+      const long long row = i / H, col = i % H;
+      const long long b = row / 256, q = row % 256;
+      const long long dst_row = b * 128 + (q % 128);
+      (q < 128 ? dw1 : dw3)[dst_row * H + col] = v;
+    } else {
+      dw2[i - n13] = v;
+    }
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+#define FSEP_CH_SWITCH(CHV, ...)                                                         \
+  switch (CHV) {                                                                         \
+    case 1: { constexpr int CH = 1; __VA_ARGS__; } break;                                \
+    case 2: { constexpr int CH = 2; __VA_ARGS__; } break;                                \
+    case 4: { constexpr int CH = 4; __VA_ARGS__; } break;                                \
+    case 8: { constexpr int CH = 8; __VA_ARGS__; } break;                                \
+    case 16: { constexpr int CH = 16; __VA_ARGS__; } break;                              \
+    default: throw std::runtime_error("hidden size must be 256 * {1,2,4,8,16}");         \
+  }
+
+void launch_router(const RouterArgs& a, cudaStream_t st) {
+  const int nblk = (a.T + kBlockTokens - 1) / kBlockTokens;
+  if (nblk == 0) return;
+  FSEP_CH_SWITCH(a.H / 256, router_kernel<CH><<<nblk, 128, 0, st>>>(a.x, a.wg, a.bias, a.T, a.E, a.K, a.topk_idx,
+                                                                     a.topk_w, a.intra_rank, a.blk_hist));
+  count_launch();
+}
+
+void launch_block_scan(const int* blk_hist, int nblk, int E, int* blk_base, const PeerTable& peers, int rank,
+                       int world, cudaStream_t st) {
+  block_scan_kernel<<<1, 128, 0, st>>>(blk_hist, nblk, E, blk_base, peers, rank, world);
+  count_launch();
+}
+
+void launch_plan(const unsigned long long* R_all, const uint8_t* layout, int E, int N, int rank, PlanTables* pt,
+                 long long row_capacity, cudaStream_t st) {
+  plan_kernel<<<1, 128, 0, st>>>(R_all, layout, E, N, rank, pt, row_capacity);
+  count_launch();
+}
+
+void launch_zero_pad(const PlanTables* pt, int C, int H, __nv_bfloat16* x_rows, __nv_bfloat16* dy_rows,
+                     cudaStream_t st) {
+  zero_pad_kernel<<<dim3(16, C), 256, 0, st>>>(pt, C, H, x_rows, dy_rows);
+  count_launch();
+}
+
+void launch_dispatch(const DispatchArgs& a, cudaStream_t st) {
+  if (a.T == 0) return;
+  FSEP_CH_SWITCH(a.H / 256, dispatch_kernel<CH><<<(a.T + 7) / 8, 256, 0, st>>>(
+                                a.x, a.T, a.K, a.E, a.topk_idx, a.intra_rank, a.blk_base, a.pt, a.peers, a.slot_dst));
+  count_launch();
+}
+
+void launch_combine(int T, int H, int K, const float* topk_w, const uint32_t* slot_dst, const PeerTable& peers,
+                    __nv_bfloat16* out, cudaStream_t st) {
+  if (T == 0) return;
+  FSEP_CH_SWITCH(H / 256, combine_kernel<CH><<<(T + 7) / 8, 256, 0, st>>>(T, K, topk_w, slot_dst, peers, out));
+  count_launch();
+}
+
+void launch_combine_bwd(int T, int H, int K, const __nv_bfloat16* dout, const float* topk_w, const uint32_t* slot_dst,
+                        const PeerTable& peers, float* dl, cudaStream_t st) {
+  if (T == 0) return;
+  FSEP_CH_SWITCH(H / 256,
+                 combine_bwd_kernel<CH><<<(T + 7) / 8, 256, 0, st>>>(T, K, dout, topk_w, slot_dst, peers, dl));
+  count_launch();
+}
+
+void launch_unpermute_bwd(int T, int H, int K, const int* topk_idx, const float* dl, const uint32_t* slot_dst,
+                          const __nv_bfloat16* wg, const PeerTable& peers, __nv_bfloat16* dx, cudaStream_t st) {
+  if (T == 0) return;
+  FSEP_CH_SWITCH(H / 256, unpermute_bwd_kernel<CH><<<(T + 7) / 8, 256, 0, st>>>(T, K, topk_idx, dl, slot_dst, wg,
+                                                                                 peers, dx));
+  count_launch();
+}
+
+int router_wgrad_splits(int T) { return T == 0 ? 1 : (T + 255) / 256; }
+
+void launch_router_wgrad(const __nv_bfloat16* x, int T, int H, int K, int E, const int* topk_idx, const float* dl,
+                         float* partial, float* dwg, cudaStream_t st) {
+  const int splits = router_wgrad_splits(T);
+  const size_t smem = static_cast<size_t>(E) * 256 * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(router_wgrad_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+    attr = true;
+  }
+  router_wgrad_partial_kernel<<<dim3(H / 256, splits), 256, smem, st>>>(x, T, H, K, E, topk_idx, dl, 256, partial);
+  router_wgrad_reduce_kernel<<<(E * H + 255) / 256, 256, 0, st>>>(partial, splits, E * H, dwg);
+  count_launch(2);
+}
+
+void launch_grad_reduce_scatter(const PlanTables* pt, const PeerTable& peers, int E, int rank, long long S,
+                                long long flat, float* grad_shard, cudaStream_t st) {
+  grad_reduce_scatter_kernel<<<dim3(64, E), 256, 0, st>>>(pt, peers, E, rank, S, flat, grad_shard);
+  count_launch();
+}
+
+void launch_pack_expert(const __nv_bfloat16* w1, const __nv_bfloat16* w3, const __nv_bfloat16* w2, int H, int F,
+                        __nv_bfloat16* flat, cudaStream_t st) {
+  pack_expert_kernel<<<1024, 256, 0, st>>>(w1, w3, w2, H, F, flat);
+  count_launch();
+}
+
+void launch_unpack_grad(const float* chunk, long long lo, long long hi, int H, int F, float* dw1, float* dw3,
+                        float* dw2, cudaStream_t st) {
+  unpack_grad_kernel<<<1024, 256, 0, st>>>(chunk, lo, hi, H, F, dw1, dw3, dw2);
+  count_launch();
+}
+
+}  // namespace fsep

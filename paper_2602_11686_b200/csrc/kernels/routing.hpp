@@ -1,0 +1,64 @@
+// Launchers of the routing / dispatch / combine kernels (routing.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels/fsep_types.cuh"
+
+namespace fsep {
+
+struct RouterArgs {
+  const __nv_bfloat16* x;
+  const __nv_bfloat16* wg;
+  const float* bias;
+  int T, H, E, K;
+  int* topk_idx;
+  float* topk_w;
+  int* intra_rank;
+  int* blk_hist;
+};
+
+struct DispatchArgs {
+  const __nv_bfloat16* x;
+  int T, H, K, E;
+  const int* topk_idx;
+  const int* intra_rank;
+  const int* blk_base;
+  const PlanTables* pt;
+  PeerTable peers;
+  uint32_t* slot_dst;
+};
+
+void launch_router(const RouterArgs& a, cudaStream_t st);
+void launch_block_scan(const int* blk_hist, int nblk, int E, int* blk_base, const PeerTable& peers, int rank,
+                       int world, cudaStream_t st);
+void launch_plan(const unsigned long long* R_all, const uint8_t* layout, int E, int N, int rank, PlanTables* pt,
+                 long long row_capacity, cudaStream_t st);
+void launch_zero_pad(const PlanTables* pt, int C, int H, __nv_bfloat16* x_rows, __nv_bfloat16* dy_rows,
+                     cudaStream_t st);
+void launch_dispatch(const DispatchArgs& a, cudaStream_t st);
+void launch_combine(int T, int H, int K, const float* topk_w, const uint32_t* slot_dst, const PeerTable& peers,
+                    __nv_bfloat16* out, cudaStream_t st);
+void launch_combine_bwd(int T, int H, int K, const __nv_bfloat16* dout, const float* topk_w, const uint32_t* slot_dst,
+                        const PeerTable& peers, float* dl, cudaStream_t st);
+void launch_unpermute_bwd(int T, int H, int K, const int* topk_idx, const float* dl, const uint32_t* slot_dst,
+                          const __nv_bfloat16* wg, const PeerTable& peers, __nv_bfloat16* dx, cudaStream_t st);
+int router_wgrad_splits(int T);
+void launch_router_wgrad(const __nv_bfloat16* x, int T, int H, int K, int E, const int* topk_idx, const float* dl,
+                         float* partial, float* dwg, cudaStream_t st);
+void launch_grad_reduce_scatter(const PlanTables* pt, const PeerTable& peers, int E, int rank, long long S,
+                                long long flat, float* grad_shard, cudaStream_t st);
+void launch_pack_expert(const __nv_bfloat16* w1, const __nv_bfloat16* w3, const __nv_bfloat16* w2, int H, int F,
+                        __nv_bfloat16* flat, cudaStream_t st);
+void launch_unpack_grad(const float* chunk, long long lo, long long hi, int H, int F, float* dw1, float* dw3,
+                        float* dw2, cudaStream_t st);
+
+void launch_restore(const uint8_t* layout, int E, int N, int rank, int C, long long S, long long flat,
+                    const PeerTable& peers, __nv_bfloat16* restored, int blocks_per_chunk, cudaStream_t st);
+
+// Cross-rank barrier for real multi-GPU mode (system-scope flags in peer memory).
+void launch_peer_barrier(unsigned int* const* peer_flags, int world, int rank, unsigned int epoch, cudaStream_t st);
+
+}  // namespace fsep

@@ -1,0 +1,42 @@
+// Test-only C entry point: runs one grouped tcgen05 GEMM on caller-provided
+// device buffers so the kernel can be checked in isolation against a torch fp32
+// matmul (tests/test_gpu_gemm.py).  Not used by the layer step.
+#include "host/capi_common.hpp"
+#include "kernels/kernels.hpp"
+#include "moeplan_fsep.h"
+
+extern "C" {
+
+// b_d0/b_d1/b_groups/b_pitch1/b_pitch2 describe B: for the M-grouped kinds a 3-D
+// bf16 tensor [groups][d1][d0] (pitches in elements); for the wgrad kind a 2-D
+// tensor [b_d1 rows][b_d0] with pitch b_pitch1.
+__attribute__((visibility("default"))) mp_status mp_fsep_debug_grouped_gemm(
+    int kind, int num_groups, const int* group_rows, const int* group_off, int M, int N, int K, const void* A,
+    unsigned long long a_rows, unsigned long long a_inner, unsigned long long a_pitch, const void* B,
+    unsigned long long b_d0, unsigned long long b_d1, unsigned long long b_groups, unsigned long long b_pitch1,
+    unsigned long long b_pitch2, void* out, long long ldo, long long out_gstride, void* out2, long long ldo2,
+    const void* aux, long long ld_aux, void* stream) {
+  using namespace fsep;
+  return moeplan::capi::guarded([&] {
+    const GemmKind k = static_cast<GemmKind>(kind);
+    const bool a_mn = k == GemmKind::kBwdWgrad;
+    const bool b_mn = k != GemmKind::kFwdGateUp && k != GemmKind::kFwdDown;
+    CUtensorMap ta = a_mn ? make_tmap_2d(A, a_inner, a_rows, a_pitch, 64, 64) : make_tmap_2d(A, a_inner, a_rows, a_pitch, 64, 128);
+    CUtensorMap tb;
+    if (k == GemmKind::kBwdWgrad)
+      tb = make_tmap_2d(B, b_d0, b_d1, b_pitch1, 64, 64);
+    else if (b_mn)
+      tb = make_tmap_3d(B, b_d0, b_d1, b_groups, b_pitch1, b_pitch2, 64, 64);
+    else
+      tb = make_tmap_3d(B, b_d0, b_d1, b_groups, b_pitch1, b_pitch2, 64, 256);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    GroupedGemmArgs g{num_groups, group_rows, group_off, M, N, K, out, ldo, out_gstride, out2, ldo2, aux, ld_aux};
+    launch_grouped_gemm(k, ta, tb, g, sms, static_cast<cudaStream_t>(stream));
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw moeplan::Error(moeplan::ErrorKind::device, cudaGetErrorString(e));
+  });
+}
+
+}  // extern "C"

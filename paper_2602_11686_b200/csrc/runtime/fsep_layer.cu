@@ -1,0 +1,755 @@
+// FsepLayer: the B200 runtime of one FSEP MoE layer step, behind the
+// mp_fsep_layer_* C ABI (include/moeplan_fsep.h).
+//
+// Step schedule (per rank; in virtual mode every phase loops over the N
+// emulated ranks on one GPU, in real mode a peer barrier separates phases):
+//   forward   layout H2D (from the planner) | restore (side stream, peer reads)
+//             router+top-k+histogram -> block scan (R row -> every rank's R_all)
+//             == barrier ==  plan (device lite routing) + pad zeroing
+//             dispatch (token rows -> destination rows, peer stores)
+//             == barrier ==  [wait restore] GEMM gate/up + SwiGLU -> GEMM down
+//             == barrier ==  combine (peer loads, gate-weighted fp32 sum)
+//             R D2H + host planner callback (planner stream) -> layout of step t+1
+//   backward  combine bwd (dw, dl; dY rows -> expert devices)
+//             == barrier ==  dgrad (SwiGLU') x2, wgrad x2 (fp32)
+//             == barrier ==  unpermute bwd (+ router dx), router wgrad,
+//             grad reduce-scatter into the fp32 shards (peer loads)
+// Nothing in the step needs a host synchronisation: the layout travels
+// host->device as a stream-ordered copy, the per-expert row counts never leave
+// the device (the grouped GEMMs schedule their tiles from them).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host/capi_common.hpp"
+#include "kernels/kernels.hpp"
+#include "kernels/routing.hpp"
+#include "moeplan/planner.hpp"
+#include "moeplan_fsep.h"
+
+using moeplan::Error;
+using moeplan::ErrorKind;
+
+namespace fsep {
+namespace {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error(ErrorKind::device, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Carver {
+  char* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    off = align_up(off, 256);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+struct Rank {
+  int rank = 0;
+  // peer-visible arena
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+  __nv_bfloat16 *x_rows = nullptr, *y_rows = nullptr, *dy_rows = nullptr, *dx_rows = nullptr;
+  unsigned long long* R_all = nullptr;
+  float* grad_full = nullptr;
+  __nv_bfloat16* shard = nullptr;
+  unsigned int* flags = nullptr;
+  // private
+  void* priv = nullptr;
+  float* grad_shard = nullptr;
+  __nv_bfloat16* restored = nullptr;
+  __nv_bfloat16 *h = nullptr, *act = nullptr, *dh = nullptr;
+  __nv_bfloat16* wg = nullptr;
+  float *dwg = nullptr, *dwg_partial = nullptr;
+  int *topk_idx = nullptr, *intra_rank = nullptr, *blk_hist = nullptr, *blk_base = nullptr;
+  float *topk_w = nullptr, *dl = nullptr;
+  uint32_t* slot_dst = nullptr;
+  uint8_t* layout_dev = nullptr;
+  PlanTables* pt = nullptr;
+  CUtensorMap tm_x_k{}, tm_w13_k{}, tm_act_k{}, tm_w2_k{}, tm_dy_k{}, tm_w2_mn{}, tm_dh_k{}, tm_w13_mn{}, tm_dy_mn{},
+      tm_act_mn{}, tm_dh_mn{}, tm_x_mn{};
+  // per-step inputs
+  const __nv_bfloat16* x_in = nullptr;
+};
+
+}  // namespace
+}  // namespace fsep
+
+using namespace fsep;
+
+extern "C" struct mp_fsep_layer {
+  mp_fsep_desc d{};
+  int device = 0;
+  int num_sms = 148;
+  int N = 1, E = 0, K = 0, H = 0, F = 0, C = 0, T_max = 0;
+  long long S = 0, flat = 0;
+  long long cap = 0;
+  bool virt = false;
+  std::vector<Rank> ranks;  // local ranks (N in virtual mode, 1 in real mode)
+  PeerTable peers{};
+  unsigned int** d_peer_flags = nullptr;
+  std::vector<cudaIpcMemHandle_t> opened;  // for bookkeeping
+  std::vector<void*> opened_ptrs;
+  bool connected = false;
+  unsigned int epoch = 0;
+  // layout / planner
+  uint8_t* layout_host = nullptr;  // pinned E*N
+  unsigned long long* R_host = nullptr;  // pinned N*E
+  mp_fsep_planner* planner = nullptr;
+  bool planner_pending = false;
+  // streams / events
+  cudaStream_t side = nullptr, plan_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_restored = nullptr, ev_hist = nullptr, ev_planned = nullptr;
+  cudaEvent_t ev_g[8] = {};
+  int T_step = 0;
+  bool restore_every_step = true;
+  // graph
+  cudaGraphExec_t graph = nullptr;
+  const void* graph_key[5] = {};
+  uint64_t launches_before = 0, launches_step = 0;
+  double gemm_flops_step = 0.0;
+};
+
+namespace {
+
+using Layer = mp_fsep_layer;
+
+void build_maps(Layer& L, Rank& r) {
+  const int H = L.H, F = L.F, C = L.C;
+  const uint64_t cap = static_cast<uint64_t>(L.cap);
+  r.tm_x_k = make_tmap_2d(r.x_rows, H, cap, H, 64, 128);
+  r.tm_act_k = make_tmap_2d(r.act, F, cap, F, 64, 128);
+  r.tm_dy_k = make_tmap_2d(r.dy_rows, H, cap, H, 64, 128);
+  r.tm_dh_k = make_tmap_2d(r.dh, 2 * F, cap, 2 * F, 64, 128);
+  r.tm_dy_mn = make_tmap_2d(r.dy_rows, H, cap, H, 64, 64);
+  r.tm_act_mn = make_tmap_2d(r.act, F, cap, F, 64, 64);
+  r.tm_dh_mn = make_tmap_2d(r.dh, 2 * F, cap, 2 * F, 64, 64);
+  r.tm_x_mn = make_tmap_2d(r.x_rows, H, cap, H, 64, 64);
+  const __nv_bfloat16* w13 = r.restored;
+  const __nv_bfloat16* w2 = r.restored + 2LL * F * H;
+  r.tm_w13_k = make_tmap_3d(w13, H, 2 * F, C, H, L.flat, 64, 256);
+  r.tm_w2_k = make_tmap_3d(w2, F, H, C, F, L.flat, 64, 256);
+  r.tm_w2_mn = make_tmap_3d(w2, F, H, C, F, L.flat, 64, 64);
+  r.tm_w13_mn = make_tmap_3d(w13, H, 2 * F, C, H, L.flat, 64, 64);
+}
+
+void allocate_rank(Layer& L, Rank& r) {
+  const size_t H = L.H, F = L.F, E = L.E, C = L.C, N = L.N, T = L.T_max, K = L.K;
+  const size_t cap = static_cast<size_t>(L.cap);
+  const size_t S = static_cast<size_t>(L.S), flat = static_cast<size_t>(L.flat);
+  const size_t nblk = (T + kBlockTokens - 1) / kBlockTokens;
+  // arena (peer-visible)
+  size_t a = 0;
+  auto acc = [&](size_t bytes) { a = align_up(a, 256) + bytes; };
+  acc(cap * H * 2);  // x_rows
+  acc(cap * H * 2);  // y_rows
+  acc(cap * H * 2);  // dy_rows
+  acc(cap * H * 2);  // dx_rows
+  acc(N * E * 8);    // R_all
+  acc(C * flat * 4);  // grad_full
+  acc(E * S * 2);    // shard
+  acc((N + 1) * 4);  // flags
+  r.arena_bytes = align_up(a, 2 << 20);
+  CK(cudaMalloc(&r.arena, r.arena_bytes));
+  CK(cudaMemset(r.arena, 0, r.arena_bytes));
+  Carver ca{static_cast<char*>(r.arena)};
+  r.x_rows = ca.take<__nv_bfloat16>(cap * H);
+  r.y_rows = ca.take<__nv_bfloat16>(cap * H);
+  r.dy_rows = ca.take<__nv_bfloat16>(cap * H);
+  r.dx_rows = ca.take<__nv_bfloat16>(cap * H);
+  r.R_all = ca.take<unsigned long long>(N * E);
+  r.grad_full = ca.take<float>(C * flat);
+  r.shard = ca.take<__nv_bfloat16>(E * S);
+  r.flags = ca.take<unsigned int>(N + 1);
+  // private
+  const int splits = router_wgrad_splits(static_cast<int>(T));
+  size_t b = 0;
+  auto accp = [&](size_t bytes) { b = align_up(b, 256) + bytes; };
+  const bool multi = N > 1;
+  if (multi) {
+    accp(E * S * 4);       // grad_shard
+    accp(C * flat * 2);    // restored
+  }
+  accp(cap * 2 * F * 2);  // h
+  accp(cap * F * 2);      // act
+  accp(cap * 2 * F * 2);  // dh
+  accp(E * H * 2);        // wg
+  accp(E * H * 4);        // dwg
+  accp(static_cast<size_t>(splits) * E * H * 4);  // dwg_partial
+  accp(T * K * 4 * 5);    // topk_idx, intra_rank, topk_w, dl, slot_dst
+  accp(nblk * E * 4 * 2);  // blk_hist, blk_base
+  accp(E * N);            // layout
+  accp(sizeof(PlanTables));
+  CK(cudaMalloc(&r.priv, align_up(b, 2 << 20)));
+  CK(cudaMemset(r.priv, 0, align_up(b, 2 << 20)));
+  Carver cp{static_cast<char*>(r.priv)};
+  if (multi) {
+    r.grad_shard = cp.take<float>(E * S);
+    r.restored = cp.take<__nv_bfloat16>(C * flat);
+  } else {
+    r.grad_shard = r.grad_full;  // one device: the shard IS the full expert set (C == E)
+    r.restored = r.shard;
+  }
+  r.h = cp.take<__nv_bfloat16>(cap * 2 * F);
+  r.act = cp.take<__nv_bfloat16>(cap * F);
+  r.dh = cp.take<__nv_bfloat16>(cap * 2 * F);
+  r.wg = cp.take<__nv_bfloat16>(E * H);
+  r.dwg = cp.take<float>(E * H);
+  r.dwg_partial = cp.take<float>(static_cast<size_t>(splits) * E * H);
+  r.topk_idx = cp.take<int>(T * K);
+  r.intra_rank = cp.take<int>(T * K);
+  r.topk_w = cp.take<float>(T * K);
+  r.dl = cp.take<float>(T * K);
+  r.slot_dst = cp.take<uint32_t>(T * K);
+  r.blk_hist = cp.take<int>(nblk * E);
+  r.blk_base = cp.take<int>(nblk * E);
+  r.layout_dev = cp.take<uint8_t>(E * N);
+  r.pt = cp.take<PlanTables>(1);
+  build_maps(L, r);
+}
+
+void finish_peers(Layer& L) {
+  // virtual mode: all ranks local; real mode: filled by connect()
+  if (L.virt) {
+    for (int p = 0; p < L.N; ++p) {
+      Rank& r = L.ranks[p];
+      L.peers.x_rows[p] = r.x_rows;
+      L.peers.y_rows[p] = r.y_rows;
+      L.peers.dy_rows[p] = r.dy_rows;
+      L.peers.dx_rows[p] = r.dx_rows;
+      L.peers.R_all[p] = r.R_all;
+      L.peers.grad_full[p] = r.grad_full;
+      L.peers.shard[p] = r.shard;
+    }
+  }
+  L.peers.row_capacity = static_cast<uint64_t>(L.cap);
+}
+
+void barrier(Layer& L, cudaStream_t st) {
+  if (L.virt || L.N == 1) return;  // stream order is the barrier on one GPU
+  launch_peer_barrier(L.d_peer_flags, L.N, L.ranks[0].rank, ++L.epoch, st);
+}
+
+GroupedGemmArgs gemm_args(Layer& L, Rank& r) {
+  GroupedGemmArgs g{};
+  g.num_groups = L.C;
+  g.group_rows = r.pt->seg_rows_pad;
+  g.group_off = r.pt->seg_off;
+  return g;
+}
+
+void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __nv_bfloat16* y, cudaStream_t st) {
+  if (T < 0 || T > L.T_max) throw Error(ErrorKind::invalid_argument, "forward: n_tokens exceeds max_tokens");
+  const int E = L.E, K = L.K, H = L.H, F = L.F, N = L.N, C = L.C;
+  L.T_step = T;
+  const long long TH = static_cast<long long>(T) * H;
+  // 1. layout for this step (planner result of the previous step, or set_layout)
+  if (L.planner_pending) CK(cudaStreamWaitEvent(st, L.ev_planned, 0));
+  for (Rank& r : L.ranks) CK(cudaMemcpyAsync(r.layout_dev, L.layout_host, static_cast<size_t>(E) * N, cudaMemcpyHostToDevice, st));
+  // 2. shard restore on the side stream (overlaps router + dispatch)
+  const bool restore = N > 1 && L.restore_every_step;
+  if (restore) {
+    CK(cudaEventRecord(L.ev_fork, st));
+    CK(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
+    for (Rank& r : L.ranks)
+      launch_restore(r.layout_dev, E, N, r.rank, C, L.S, L.flat, L.peers, r.restored, 16, L.side);
+    CK(cudaEventRecord(L.ev_restored, L.side));
+  }
+  // 3. router + top-k + histogram, global ranks, R exchange
+  const int nblk = (T + kBlockTokens - 1) / kBlockTokens;
+  for (size_t v = 0; v < L.ranks.size(); ++v) {
+    Rank& r = L.ranks[v];
+    r.x_in = x + (L.virt ? static_cast<long long>(v) * TH : 0);
+    const float* b = bias ? bias + (L.virt ? static_cast<long long>(v) * T * E : 0) : nullptr;
+    launch_router(RouterArgs{r.x_in, r.wg, b, T, H, E, K, r.topk_idx, r.topk_w, r.intra_rank, r.blk_hist}, st);
+    launch_block_scan(r.blk_hist, nblk, E, r.blk_base, L.peers, r.rank, N, st);
+  }
+  barrier(L, st);
+  // 4. device lite routing + receive layout; dispatch
+  for (Rank& r : L.ranks) {
+    launch_plan(r.R_all, r.layout_dev, E, N, r.rank, r.pt, L.cap, st);
+    launch_zero_pad(r.pt, C, H, r.x_rows, r.dy_rows, st);
+  }
+  // histogram -> host planner (async, off the critical path)
+  CK(cudaMemcpyAsync(L.R_host, L.ranks[0].R_all, static_cast<size_t>(N) * E * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(L.ev_hist, st));
+  if (L.planner) {
+    CK(cudaStreamWaitEvent(L.plan_stream, L.ev_hist, 0));
+    CK(cudaLaunchHostFunc(
+        L.plan_stream,
+        [](void* p) {
+          Layer* l = static_cast<Layer*>(p);
+          // errors cannot propagate from a host node; keep the previous layout on failure
+          if (mp_fsep_planner_observe(l->planner, reinterpret_cast<const uint64_t*>(l->R_host)) == MP_OK) mp_fsep_planner_next(l->planner, l->layout_host);
+        },
+        &L));
+    CK(cudaEventRecord(L.ev_planned, L.plan_stream));
+    L.planner_pending = true;
+  }
+  for (Rank& r : L.ranks)
+    launch_dispatch(DispatchArgs{r.x_in, T, H, K, E, r.topk_idx, r.intra_rank, r.blk_base, r.pt, L.peers, r.slot_dst}, st);
+  barrier(L, st);
+  // 5. expert FFN on the restored experts
+  if (restore) CK(cudaStreamWaitEvent(st, L.ev_restored, 0));
+  CK(cudaEventRecord(L.ev_g[0], st));
+  for (Rank& r : L.ranks) {
+    GroupedGemmArgs g = gemm_args(L, r);
+    g.N = 2 * F;
+    g.K = H;
+    g.out = r.h;
+    g.ldo = 2 * F;
+    g.out2 = r.act;
+    g.ldo2 = F;
+    launch_grouped_gemm(GemmKind::kFwdGateUp, r.tm_x_k, r.tm_w13_k, g, L.num_sms, st);
+    GroupedGemmArgs g2 = gemm_args(L, r);
+    g2.N = H;
+    g2.K = F;
+    g2.out = r.y_rows;
+    g2.ldo = H;
+    launch_grouped_gemm(GemmKind::kFwdDown, r.tm_act_k, r.tm_w2_k, g2, L.num_sms, st);
+  }
+  CK(cudaEventRecord(L.ev_g[1], st));
+  barrier(L, st);
+  // 6. combine
+  for (size_t v = 0; v < L.ranks.size(); ++v) {
+    Rank& r = L.ranks[v];
+    launch_combine(T, H, K, r.topk_w, r.slot_dst, L.peers, y + (L.virt ? static_cast<long long>(v) * TH : 0), st);
+  }
+}
+
+void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStream_t st) {
+  const int E = L.E, K = L.K, H = L.H, F = L.F, N = L.N, T = L.T_step;
+  const long long TH = static_cast<long long>(T) * H;
+  for (size_t v = 0; v < L.ranks.size(); ++v) {
+    Rank& r = L.ranks[v];
+    launch_combine_bwd(T, H, K, dy + (L.virt ? static_cast<long long>(v) * TH : 0), r.topk_w, r.slot_dst, L.peers,
+                       r.dl, st);
+  }
+  barrier(L, st);
+  CK(cudaEventRecord(L.ev_g[2], st));
+  for (Rank& r : L.ranks) {
+    GroupedGemmArgs g = gemm_args(L, r);  // dAct -> dH (SwiGLU backward fused)
+    g.N = F;
+    g.K = H;
+    g.out = r.dh;
+    g.ldo = 2 * F;
+    g.aux = r.h;
+    g.ld_aux = 2 * F;
+    launch_grouped_gemm(GemmKind::kBwdDownDgrad, r.tm_dy_k, r.tm_w2_mn, g, L.num_sms, st);
+    GroupedGemmArgs g2 = gemm_args(L, r);  // dX rows
+    g2.N = H;
+    g2.K = 2 * F;
+    g2.out = r.dx_rows;
+    g2.ldo = H;
+    launch_grouped_gemm(GemmKind::kBwdUpDgrad, r.tm_dh_k, r.tm_w13_mn, g2, L.num_sms, st);
+    GroupedGemmArgs g3 = gemm_args(L, r);  // dW2 = dY^T act
+    g3.M = H;
+    g3.N = F;
+    g3.out = r.grad_full + 2LL * F * H;
+    g3.ldo = F;
+    g3.out_group_stride = L.flat;
+    launch_grouped_gemm(GemmKind::kBwdWgrad, r.tm_dy_mn, r.tm_act_mn, g3, L.num_sms, st);
+    GroupedGemmArgs g4 = gemm_args(L, r);  // dW13 = dH^T X
+    g4.M = 2 * F;
+    g4.N = H;
+    g4.out = r.grad_full;
+    g4.ldo = H;
+    g4.out_group_stride = L.flat;
+    launch_grouped_gemm(GemmKind::kBwdWgrad, r.tm_dh_mn, r.tm_x_mn, g4, L.num_sms, st);
+  }
+  CK(cudaEventRecord(L.ev_g[3], st));
+  barrier(L, st);
+  for (size_t v = 0; v < L.ranks.size(); ++v) {
+    Rank& r = L.ranks[v];
+    launch_unpermute_bwd(T, H, K, r.topk_idx, r.dl, r.slot_dst, r.wg, L.peers,
+                         dx + (L.virt ? static_cast<long long>(v) * TH : 0), st);
+    launch_router_wgrad(r.x_in, T, H, K, E, r.topk_idx, r.dl, r.dwg_partial, r.dwg, st);
+  }
+  if (N > 1)
+    for (Rank& r : L.ranks) launch_grad_reduce_scatter(r.pt, L.peers, E, r.rank, L.S, L.flat, r.grad_shard, st);
+  // join the planner stream (it finished long before the backward GEMMs did)
+  if (L.planner_pending) CK(cudaStreamWaitEvent(st, L.ev_planned, 0));
+}
+
+Rank& rank_of(Layer& L, uint32_t vrank) {
+  if (!L.virt) return L.ranks[0];
+  if (vrank >= L.ranks.size()) throw Error(ErrorKind::invalid_argument, "vrank out of range");
+  return L.ranks[vrank];
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+using moeplan::capi::guarded;
+using moeplan::capi::require;
+
+extern "C" {
+
+mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_layer** out) {
+  return guarded([&] {
+    require(desc && out, "mp_fsep_layer_create: NULL argument");
+    const mp_fsep_desc& d = *desc;
+    require(d.world >= 1 && d.world <= static_cast<uint32_t>(kMaxRanks), "world must be in [1, 16]");
+    require(d.n_experts >= 1 && d.n_experts <= static_cast<uint32_t>(kMaxExperts), "n_experts must be in [1, 128]");
+    require(d.top_k >= 1 && d.top_k <= 8 && d.top_k <= d.n_experts, "top_k must be in [1, min(8, E)]");
+    require(d.hidden % 256 == 0 && d.hidden >= 256 && d.hidden <= 4096, "hidden must be 256*{1,2,4,8,16}");
+    require((d.hidden & (d.hidden - 1)) == 0, "hidden must be 256*{1,2,4,8,16}");
+    require(d.ffn % 128 == 0 && d.ffn > 0, "ffn must be a multiple of 128");
+    require(d.capacity >= 1 && d.capacity <= d.n_experts && d.n_experts <= d.world * d.capacity,
+            "capacity must satisfy 1 <= C <= E <= N*C");
+    require(d.top_k <= d.capacity * d.world, "top_k too large");
+    require(d.virtual_ranks || d.rank < d.world, "rank out of range");
+    const long long flat = 3LL * d.hidden * d.ffn;
+    require(flat % (8LL * d.world) == 0, "3*H*F must be divisible by 8*world (16-byte shard chunks)");
+    auto L = std::make_unique<mp_fsep_layer>();
+    L->d = d;
+    L->device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceGetAttribute(&L->num_sms, cudaDevAttrMultiProcessorCount, device));
+    L->N = static_cast<int>(d.world);
+    L->E = static_cast<int>(d.n_experts);
+    L->K = static_cast<int>(d.top_k);
+    L->H = static_cast<int>(d.hidden);
+    L->F = static_cast<int>(d.ffn);
+    L->C = static_cast<int>(d.capacity);
+    L->T_max = static_cast<int>(d.max_tokens);
+    L->flat = flat;
+    L->S = flat / L->N;
+    L->virt = d.virtual_ranks != 0 || L->N == 1;
+    const long long worst = static_cast<long long>(d.max_tokens) * d.top_k * L->N + 128LL * L->C;
+    L->cap = d.max_recv_rows ? static_cast<long long>(d.max_recv_rows) + 128LL * L->C : worst;
+    require(L->cap < (1LL << 24), "receive rows must stay below 2^24");
+    const int local = L->virt ? L->N : 1;
+    L->ranks.resize(local);
+    for (int v = 0; v < local; ++v) {
+      L->ranks[v].rank = L->virt ? v : static_cast<int>(d.rank);
+      allocate_rank(*L, L->ranks[v]);
+    }
+    finish_peers(*L);
+    L->connected = L->virt;
+    CK(cudaMallocHost(&L->layout_host, static_cast<size_t>(L->E) * L->N));
+    CK(cudaMallocHost(&L->R_host, static_cast<size_t>(L->E) * L->N * 8));
+    // default layout: even replication (sim.cpp:100-103 initial layout)
+    require(mp_fsep_even_layout(L->N, L->E, L->C, L->layout_host) == MP_OK, "even layout failed");
+    CK(cudaStreamCreateWithFlags(&L->side, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&L->plan_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&L->ev_fork, &L->ev_restored, &L->ev_hist, &L->ev_planned})
+      CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    for (auto& e : L->ev_g) CK(cudaEventCreate(&e));
+    CK(cudaMalloc(&L->d_peer_flags, sizeof(unsigned int*) * kMaxRanks));
+    if (L->virt) {
+      unsigned int* f[kMaxRanks] = {};
+      for (int v = 0; v < local; ++v) f[v] = L->ranks[v].flags;
+      CK(cudaMemcpy(L->d_peer_flags, f, sizeof(f), cudaMemcpyHostToDevice));
+    }
+    CK(cudaDeviceSynchronize());
+    *out = L.release();
+  });
+}
+
+void mp_fsep_layer_free(mp_fsep_layer* L) {
+  if (!L) return;
+  cudaSetDevice(L->device);
+  cudaDeviceSynchronize();
+  if (L->graph) cudaGraphExecDestroy(L->graph);
+  for (void* p : L->opened_ptrs) cudaIpcCloseMemHandle(p);
+  for (Rank& r : L->ranks) {
+    cudaFree(r.arena);
+    cudaFree(r.priv);
+  }
+  cudaFree(L->d_peer_flags);
+  cudaFreeHost(L->layout_host);
+  cudaFreeHost(L->R_host);
+  cudaStreamDestroy(L->side);
+  cudaStreamDestroy(L->plan_stream);
+  for (cudaEvent_t e : {L->ev_fork, L->ev_restored, L->ev_hist, L->ev_planned}) cudaEventDestroy(e);
+  for (auto e : L->ev_g) cudaEventDestroy(e);
+  delete L;
+}
+
+size_t mp_fsep_ipc_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+mp_status mp_fsep_nccl_unique_id(void* out, size_t bytes) {
+  return guarded([&] {
+    require(out && bytes >= sizeof(ncclUniqueId), "mp_fsep_nccl_unique_id: buffer too small");
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) throw Error(ErrorKind::device, "ncclGetUniqueId failed");
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+mp_status mp_fsep_layer_ipc_handle(mp_fsep_layer* L, void* out, size_t bytes) {
+  return guarded([&] {
+    require(L && out && bytes >= sizeof(cudaIpcMemHandle_t), "mp_fsep_layer_ipc_handle: bad argument");
+    require(!L->virt, "ipc handles are only used in real multi-GPU mode");
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, L->ranks[0].arena));
+    std::memcpy(out, &h, sizeof(h));
+  });
+}
+
+mp_status mp_fsep_layer_connect(mp_fsep_layer* L, const void* all_handles, const void* /*nccl_id*/) {
+  return guarded([&] {
+    require(L && all_handles, "mp_fsep_layer_connect: NULL argument");
+    require(!L->virt, "connect is only used in real multi-GPU mode");
+    CK(cudaSetDevice(L->device));
+    const auto* hs = static_cast<const cudaIpcMemHandle_t*>(all_handles);
+    Rank& me = L->ranks[0];
+    unsigned int* flags[kMaxRanks] = {};
+    for (int p = 0; p < L->N; ++p) {
+      char* base;
+      if (p == me.rank) {
+        base = static_cast<char*>(me.arena);
+      } else {
+        void* ptr = nullptr;
+        CK(cudaIpcOpenMemHandle(&ptr, hs[p], cudaIpcMemLazyEnablePeerAccess));
+        L->opened_ptrs.push_back(ptr);
+        base = static_cast<char*>(ptr);
+      }
+      // identical carving on every rank -> identical offsets
+      auto off = [&](const void* q) { return static_cast<const char*>(q) - static_cast<char*>(me.arena); };
+      L->peers.x_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.x_rows));
+      L->peers.y_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.y_rows));
+      L->peers.dy_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.dy_rows));
+      L->peers.dx_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.dx_rows));
+      L->peers.R_all[p] = reinterpret_cast<unsigned long long*>(base + off(me.R_all));
+      L->peers.grad_full[p] = reinterpret_cast<float*>(base + off(me.grad_full));
+      L->peers.shard[p] = reinterpret_cast<const __nv_bfloat16*>(base + off(me.shard));
+      flags[p] = reinterpret_cast<unsigned int*>(base + off(me.flags));
+    }
+    CK(cudaMemcpy(L->d_peer_flags, flags, sizeof(flags), cudaMemcpyHostToDevice));
+    L->connected = true;
+  });
+}
+
+mp_status mp_fsep_layer_load_expert(mp_fsep_layer* L, uint32_t expert, const void* w1, const void* w3, const void* w2,
+                                    void* stream) {
+  return guarded([&] {
+    require(L && w1 && w3 && w2, "mp_fsep_layer_load_expert: NULL argument");
+    require(expert < static_cast<uint32_t>(L->E), "expert out of range");
+    CK(cudaSetDevice(L->device));
+    auto st = static_cast<cudaStream_t>(stream);
+    const size_t n1 = static_cast<size_t>(L->F) * L->H;
+    __nv_bfloat16 *tmp = nullptr, *flat = nullptr;
+    CK(cudaMallocAsync(&tmp, 3 * n1 * 2, st));
+    CK(cudaMallocAsync(&flat, 3 * n1 * 2, st));
+    CK(cudaMemcpyAsync(tmp, w1, n1 * 2, cudaMemcpyDefault, st));
+    CK(cudaMemcpyAsync(tmp + n1, w3, n1 * 2, cudaMemcpyDefault, st));
+    CK(cudaMemcpyAsync(tmp + 2 * n1, w2, n1 * 2, cudaMemcpyDefault, st));
+    launch_pack_expert(tmp, tmp + n1, tmp + 2 * n1, L->H, L->F, flat, st);
+    for (Rank& r : L->ranks)
+      CK(cudaMemcpyAsync(r.shard + static_cast<long long>(expert) * L->S, flat + static_cast<long long>(r.rank) * L->S,
+                         static_cast<size_t>(L->S) * 2, cudaMemcpyDeviceToDevice, st));
+    CK(cudaFreeAsync(tmp, st));
+    CK(cudaFreeAsync(flat, st));
+  });
+}
+
+mp_status mp_fsep_layer_load_router(mp_fsep_layer* L, const void* wg, void* stream) {
+  return guarded([&] {
+    require(L && wg, "mp_fsep_layer_load_router: NULL argument");
+    CK(cudaSetDevice(L->device));
+    for (Rank& r : L->ranks)
+      CK(cudaMemcpyAsync(r.wg, wg, static_cast<size_t>(L->E) * L->H * 2, cudaMemcpyDefault,
+                         static_cast<cudaStream_t>(stream)));
+  });
+}
+
+mp_status mp_fsep_layer_set_layout(mp_fsep_layer* L, const uint8_t* A) {
+  return guarded([&] {
+    require(L && A, "mp_fsep_layer_set_layout: NULL argument");
+    // validate like validate_layout (types.cpp:103-113)
+    for (int d = 0; d < L->N; ++d) {
+      int held = 0;
+      for (int e = 0; e < L->E; ++e) held += A[e * L->N + d] ? 1 : 0;
+      require(held == L->C, "layout: every device must host exactly C experts");
+    }
+    for (int e = 0; e < L->E; ++e) {
+      int reps = 0;
+      for (int d = 0; d < L->N; ++d) reps += A[e * L->N + d] ? 1 : 0;
+      require(reps >= 1, "layout: every expert needs a replica");
+    }
+    if (L->planner_pending) CK(cudaEventSynchronize(L->ev_planned));  // don't race the planner callback
+    for (int i = 0; i < L->E * L->N; ++i) L->layout_host[i] = A[i] ? 1 : 0;
+  });
+}
+
+mp_status mp_fsep_layer_attach_planner(mp_fsep_layer* L, mp_fsep_planner* planner) {
+  return guarded([&] {
+    require(L, "mp_fsep_layer_attach_planner: NULL layer");
+    if (L->planner_pending) CK(cudaEventSynchronize(L->ev_planned));
+    L->planner = planner;
+    L->planner_pending = false;
+  });
+}
+
+mp_status mp_fsep_layer_forward(mp_fsep_layer* L, const void* x, const float* bias, uint32_t n_tokens, void* y,
+                                void* stream) {
+  return guarded([&] {
+    require(L && x && y, "mp_fsep_layer_forward: NULL argument");
+    require(L->connected, "mp_fsep_layer_forward: multi-GPU layer not connected");
+    CK(cudaSetDevice(L->device));
+    L->launches_before = launches_issued();
+    run_forward(*L, static_cast<const __nv_bfloat16*>(x), bias, static_cast<int>(n_tokens),
+                static_cast<__nv_bfloat16*>(y), static_cast<cudaStream_t>(stream));
+    CK(cudaGetLastError());
+  });
+}
+
+mp_status mp_fsep_layer_backward(mp_fsep_layer* L, const void* dy, void* dx, void* stream) {
+  return guarded([&] {
+    require(L && dy && dx, "mp_fsep_layer_backward: NULL argument");
+    CK(cudaSetDevice(L->device));
+    run_backward(*L, static_cast<const __nv_bfloat16*>(dy), static_cast<__nv_bfloat16*>(dx),
+                 static_cast<cudaStream_t>(stream));
+    L->launches_step = launches_issued() - L->launches_before;
+    CK(cudaGetLastError());
+  });
+}
+
+mp_status mp_fsep_layer_histogram(mp_fsep_layer* L, uint64_t* R_out) {
+  return guarded([&] {
+    require(L && R_out, "mp_fsep_layer_histogram: NULL argument");
+    CK(cudaEventSynchronize(L->ev_hist));
+    std::memcpy(R_out, L->R_host, static_cast<size_t>(L->N) * L->E * 8);
+  });
+}
+
+mp_status mp_fsep_layer_expert_grad(mp_fsep_layer* L, uint32_t expert, float* dw1, float* dw3, float* dw2,
+                                    void* stream) {
+  return guarded([&] {
+    require(L && dw1 && dw3 && dw2, "mp_fsep_layer_expert_grad: NULL argument");
+    require(expert < static_cast<uint32_t>(L->E), "expert out of range");
+    require(is_device_ptr(dw1) && is_device_ptr(dw3) && is_device_ptr(dw2), "grad outputs must be device pointers");
+    auto st = static_cast<cudaStream_t>(stream);
+    for (Rank& r : L->ranks) {
+      const long long lo = static_cast<long long>(r.rank) * L->S;
+      launch_unpack_grad(r.grad_shard + static_cast<long long>(expert) * L->S, lo, lo + L->S, L->H, L->F, dw1, dw3,
+                         dw2, st);
+    }
+  });
+}
+
+mp_status mp_fsep_layer_router_grad(mp_fsep_layer* L, uint32_t vrank, float* dwg, void* stream) {
+  return guarded([&] {
+    require(L && dwg, "mp_fsep_layer_router_grad: NULL argument");
+    Rank& r = rank_of(*L, vrank);
+    CK(cudaMemcpyAsync(dwg, r.dwg, static_cast<size_t>(L->E) * L->H * 4, cudaMemcpyDefault,
+                       static_cast<cudaStream_t>(stream)));
+  });
+}
+
+mp_status mp_fsep_layer_read(mp_fsep_layer* L, const char* name, uint32_t vrank, void* dst, uint64_t bytes,
+                             uint64_t* needed) {
+  return guarded([&] {
+    require(L && name, "mp_fsep_layer_read: NULL argument");
+    Rank& r = rank_of(*L, vrank);
+    const std::string n(name);
+    const size_t T = static_cast<size_t>(L->T_step), K = L->K, E = L->E, N = L->N, H = L->H, F = L->F, C = L->C;
+    const size_t cap = static_cast<size_t>(L->cap);
+    const void* src = nullptr;
+    size_t sz = 0;
+    if (n == "topk_idx") src = r.topk_idx, sz = T * K * 4;
+    else if (n == "topk_w") src = r.topk_w, sz = T * K * 4;
+    else if (n == "slot_dst") src = r.slot_dst, sz = T * K * 4;
+    else if (n == "dl") src = r.dl, sz = T * K * 4;
+    else if (n == "R") src = r.R_all, sz = N * E * 8;
+    else if (n == "layout") src = r.layout_dev, sz = E * N;
+    else if (n == "seg_rows") src = r.pt->seg_rows, sz = C * 4;
+    else if (n == "seg_off") src = r.pt->seg_off, sz = C * 4;
+    else if (n == "slot_expert") src = r.pt->slot_expert, sz = C * 4;
+    else if (n == "status") src = &r.pt->status, sz = 4;
+    else if (n == "total_rows") src = &r.pt->total_rows, sz = 4;
+    else if (n == "x_rows") src = r.x_rows, sz = cap * H * 2;
+    else if (n == "y_rows") src = r.y_rows, sz = cap * H * 2;
+    else if (n == "dy_rows") src = r.dy_rows, sz = cap * H * 2;
+    else if (n == "dx_rows") src = r.dx_rows, sz = cap * H * 2;
+    else if (n == "h") src = r.h, sz = cap * 2 * F * 2;
+    else if (n == "act") src = r.act, sz = cap * F * 2;
+    else if (n == "restored") src = r.restored, sz = C * static_cast<size_t>(L->flat) * 2;
+    else if (n == "grad_full") src = r.grad_full, sz = C * static_cast<size_t>(L->flat) * 4;
+    else if (n == "barrier_status") src = r.flags + N, sz = 4;
+    else throw Error(ErrorKind::invalid_argument, "mp_fsep_layer_read: unknown buffer " + n);
+    if (needed) *needed = sz;
+    if (dst) {
+      require(bytes >= sz, "mp_fsep_layer_read: destination too small");
+      CK(cudaDeviceSynchronize());
+      CK(cudaMemcpy(dst, src, sz, cudaMemcpyDefault));
+    }
+  });
+}
+
+mp_status mp_fsep_layer_stats(mp_fsep_layer* L, uint64_t* kernel_launches, double* gemm_ms, double* gemm_flops) {
+  return guarded([&] {
+    require(L, "mp_fsep_layer_stats: NULL layer");
+    CK(cudaEventSynchronize(L->ev_g[3]));
+    float f0 = 0, f1 = 0;
+    CK(cudaEventElapsedTime(&f0, L->ev_g[0], L->ev_g[1]));
+    CK(cudaEventElapsedTime(&f1, L->ev_g[2], L->ev_g[3]));
+    if (kernel_launches) *kernel_launches = L->launches_step;
+    if (gemm_ms) *gemm_ms = static_cast<double>(f0) + static_cast<double>(f1);
+    if (gemm_flops) {
+      // algorithmic FLOPs of the grouped GEMMs this step: 18*H*F per routed token-slot (fwd 6HF + bwd 12HF)
+      unsigned long long slots = 0;
+      std::vector<unsigned long long> R(static_cast<size_t>(L->N) * L->E);
+      CK(cudaMemcpy(R.data(), L->ranks[0].R_all, R.size() * 8, cudaMemcpyDeviceToHost));
+      for (auto v : R) slots += v;
+      const double local_share = L->virt ? 1.0 : 1.0 / L->N;  // real mode: report this rank's share
+      *gemm_flops = 18.0 * L->H * L->F * static_cast<double>(slots) * local_share;
+    }
+  });
+}
+
+mp_status mp_fsep_layer_graph_step(mp_fsep_layer* L, const void* x, const float* bias, uint32_t n_tokens, void* y,
+                                   const void* dy, void* dx, void* stream) {
+  return guarded([&] {
+    require(L && x && y && dy && dx, "mp_fsep_layer_graph_step: NULL argument");
+    auto st = static_cast<cudaStream_t>(stream);
+    CK(cudaSetDevice(L->device));
+    const void* key[5] = {x, bias, y, dy, dx};
+    const bool same = L->graph && std::memcmp(key, L->graph_key, sizeof(key)) == 0 && L->T_step == static_cast<int>(n_tokens);
+    if (!same) {
+      if (L->graph) cudaGraphExecDestroy(L->graph);
+      L->graph = nullptr;
+      cudaGraph_t g;
+      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      const uint64_t l0 = launches_issued();
+      try {
+        run_forward(*L, static_cast<const __nv_bfloat16*>(x), bias, static_cast<int>(n_tokens),
+                    static_cast<__nv_bfloat16*>(y), st);
+        run_backward(*L, static_cast<const __nv_bfloat16*>(dy), static_cast<__nv_bfloat16*>(dx), st);
+      } catch (...) {
+        cudaStreamEndCapture(st, &g);
+        throw;
+      }
+      L->launches_step = launches_issued() - l0;
+      CK(cudaStreamEndCapture(st, &g));
+      CK(cudaGraphInstantiate(&L->graph, g, 0));
+      CK(cudaGraphDestroy(g));
+      std::memcpy(L->graph_key, key, sizeof(key));
+    }
+    CK(cudaGraphLaunch(L->graph, st));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,166 @@
+"""FSEP MoE layer, Python side: a thin owner of an mp_fsep_layer handle.
+
+All compute runs in libmoeplan_b200.so (hand-written sm_100a kernels); torch is
+only used here to hold device tensors and streams.  There is no fallback: if the
+library or a GPU is missing, construction raises.
+
+Modes (mp_fsep_desc.virtual_ranks):
+  * real     -- one process per GPU (torch.distributed launch), world = N; ranks
+                exchange CUDA IPC handles once (connect()) and then move tokens,
+                shards and gradients with peer loads/stores over NVLink.
+  * virtual  -- all N ranks emulated on one GPU (correctness / tests); inputs
+                and outputs hold the N ranks' [T, H] blocks concatenated.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from ._lib import FsepDesc, check, load, u8p, u64p
+from .planner import Config, Planner
+
+
+@dataclass
+class LayerSpec:
+    n_experts: int
+    top_k: int
+    hidden: int
+    ffn: int
+    max_tokens: int
+    capacity: int
+    world: int = 1
+    rank: int = 0
+    virtual: bool = False
+    max_recv_rows: int = 0
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    assert t.is_contiguous()
+    return C.c_void_p(t.data_ptr())
+
+
+class FsepLayer:
+    def __init__(self, spec: LayerSpec, device: Optional[int] = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("FsepLayer needs a CUDA device (no CPU fallback)")
+        self.lib = load()
+        self.spec = spec
+        self.device = torch.cuda.current_device() if device is None else device
+        d = FsepDesc(spec.n_experts, spec.top_k, spec.hidden, spec.ffn, spec.max_tokens, spec.capacity, spec.world,
+                     spec.rank, 1 if spec.virtual else 0, 0, spec.max_recv_rows)
+        h = C.c_void_p()
+        check(self.lib.mp_fsep_layer_create(C.byref(d), self.device, C.byref(h)))
+        self._h = h
+        self._planner = None
+        self.local_ranks = spec.world if (spec.virtual or spec.world == 1) else 1
+
+    # ------------------------------------------------------------ multi-GPU
+    def ipc_handle(self) -> bytes:
+        n = self.lib.mp_fsep_ipc_bytes()
+        buf = (C.c_char * n)()
+        check(self.lib.mp_fsep_layer_ipc_handle(self._h, buf, n))
+        return bytes(buf)
+
+    def connect(self, handles: list[bytes]) -> None:
+        blob = b"".join(handles)
+        buf = (C.c_char * len(blob)).from_buffer_copy(blob)
+        check(self.lib.mp_fsep_layer_connect(self._h, buf, None))
+
+    def connect_torch_distributed(self) -> None:
+        """Exchange IPC handles with torch.distributed (any backend)."""
+        import torch.distributed as dist
+        mine = self.ipc_handle()
+        out = [None] * dist.get_world_size()
+        dist.all_gather_object(out, mine)
+        self.connect(out)
+
+    # ------------------------------------------------------------ parameters
+    def load_expert(self, e: int, w1: torch.Tensor, w3: torch.Tensor, w2: torch.Tensor, stream=None) -> None:
+        for t in (w1, w3, w2):
+            assert t.dtype == torch.bfloat16 and t.is_contiguous()
+        check(self.lib.mp_fsep_layer_load_expert(self._h, e, _ptr(w1), _ptr(w3), _ptr(w2), _stream(stream)))
+
+    def load_router(self, wg: torch.Tensor, stream=None) -> None:
+        assert wg.dtype == torch.bfloat16 and wg.is_contiguous()
+        check(self.lib.mp_fsep_layer_load_router(self._h, _ptr(wg), _stream(stream)))
+
+    def set_layout(self, A: np.ndarray) -> None:
+        A = np.ascontiguousarray(A, dtype=np.uint8)
+        check(self.lib.mp_fsep_layer_set_layout(self._h, A.ctypes.data_as(u8p)))
+
+    def attach_planner(self, config: Config, layer: int = 0) -> Planner:
+        self._planner = Planner(config, self.spec.world, layer)
+        check(self.lib.mp_fsep_layer_attach_planner(self._h, self._planner._h))
+        return self._planner
+
+    # ------------------------------------------------------------ step
+    def forward(self, x: torch.Tensor, bias: Optional[torch.Tensor], n_tokens: int, y: torch.Tensor,
+                stream=None) -> torch.Tensor:
+        check(self.lib.mp_fsep_layer_forward(self._h, _ptr(x), _ptr(bias), n_tokens, _ptr(y), _stream(stream)))
+        return y
+
+    def backward(self, dy: torch.Tensor, dx: torch.Tensor, stream=None) -> torch.Tensor:
+        check(self.lib.mp_fsep_layer_backward(self._h, _ptr(dy), _ptr(dx), _stream(stream)))
+        return dx
+
+    def graph_step(self, x, bias, n_tokens, y, dy, dx, stream=None) -> None:
+        check(self.lib.mp_fsep_layer_graph_step(self._h, _ptr(x), _ptr(bias), n_tokens, _ptr(y), _ptr(dy), _ptr(dx),
+                                                _stream(stream)))
+
+    # ------------------------------------------------------------ outputs
+    def histogram(self) -> np.ndarray:
+        R = np.zeros((self.spec.world, self.spec.n_experts), dtype=np.uint64)
+        check(self.lib.mp_fsep_layer_histogram(self._h, R.ctypes.data_as(u64p)))
+        return R
+
+    def expert_grad(self, e: int, stream=None):
+        s = self.spec
+        dw1 = torch.zeros(s.ffn, s.hidden, device="cuda", dtype=torch.float32)
+        dw3 = torch.zeros_like(dw1)
+        dw2 = torch.zeros(s.hidden, s.ffn, device="cuda", dtype=torch.float32)
+        check(self.lib.mp_fsep_layer_expert_grad(self._h, e, _ptr(dw1), _ptr(dw3), _ptr(dw2), _stream(stream)))
+        return dw1, dw3, dw2
+
+    def router_grad(self, vrank: int = 0) -> torch.Tensor:
+        s = self.spec
+        out = torch.empty(s.n_experts, s.hidden, device="cuda", dtype=torch.float32)
+        check(self.lib.mp_fsep_layer_router_grad(self._h, vrank, _ptr(out), _stream(None)))
+        return out
+
+    def read(self, name: str, vrank: int = 0) -> np.ndarray:
+        need = C.c_uint64()
+        check(self.lib.mp_fsep_layer_read(self._h, name.encode(), vrank, None, 0, C.byref(need)))
+        buf = np.empty(need.value, dtype=np.uint8)
+        check(self.lib.mp_fsep_layer_read(self._h, name.encode(), vrank, buf.ctypes.data_as(C.c_void_p),
+                                          need.value, None))
+        return buf
+
+    def stats(self):
+        n = C.c_uint64()
+        ms, fl = C.c_double(), C.c_double()
+        check(self.lib.mp_fsep_layer_stats(self._h, C.byref(n), C.byref(ms), C.byref(fl)))
+        return {"kernel_launches": n.value, "gemm_ms": ms.value, "gemm_flops": fl.value}
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            if self._planner is not None:
+                self.lib.mp_fsep_layer_attach_planner(self._h, None)
+            self.lib.mp_fsep_layer_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

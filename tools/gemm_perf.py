@@ -1,0 +1,39 @@
+"""Quick throughput probe of the grouped tcgen05 GEMM at layer shapes (dev tool)."""
+import sys, ctypes as C
+sys.path.insert(0, ".")
+import torch
+from tests.test_gpu_gemm import _run, _groups
+
+def bench(fn, iters=10):
+    for _ in range(3): fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters): fn()
+    e.record(); torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+H, F, G, rows = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+counts = [rows] * G
+rg, off, R = _groups(counts)
+X = torch.randn(R, H, device="cuda").bfloat16()
+W13 = (torch.randn(G, 2*F, H, device="cuda") / H**0.5).bfloat16()
+W2 = (torch.randn(G, H, F, device="cuda") / F**0.5).bfloat16()
+h = torch.empty(R, 2*F, device="cuda", dtype=torch.bfloat16); act = torch.empty(R, F, device="cuda", dtype=torch.bfloat16)
+y = torch.empty(R, H, device="cuda", dtype=torch.bfloat16); dY = torch.randn(R, H, device="cuda").bfloat16()
+dH = torch.empty(R, 2*F, device="cuda", dtype=torch.bfloat16); dX = torch.empty(R, H, device="cuda", dtype=torch.bfloat16)
+gW2 = torch.empty(G, H, F, device="cuda"); gW13 = torch.empty(G, 2*F, H, device="cuda")
+tests = {
+ "gateup": (lambda: _run("gateup", G, rg, off, 0, 2*F, H, X, R, H, W13, H, 2*F, G, H, 2*F*H, h, 2*F, out2=act, ldo2=F), 2*R*H*2*F),
+ "down": (lambda: _run("down", G, rg, off, 0, H, F, act, R, F, W2, F, H, G, F, H*F, y, H), 2*R*H*F),
+ "down_dgrad": (lambda: _run("down_dgrad", G, rg, off, 0, F, H, dY, R, H, W2, F, H, G, F, H*F, dH, 2*F, aux=h, ld_aux=2*F), 2*R*H*F),
+ "up_dgrad": (lambda: _run("up_dgrad", G, rg, off, 0, H, 2*F, dH, R, 2*F, W13, H, 2*F, G, H, 2*F*H, dX, H), 2*R*H*2*F),
+ "wgrad_w2": (lambda: _run("wgrad", G, rg, off, H, F, 0, dY, R, H, act, F, R, 1, F, 0, gW2, F, ogs=H*F), 2*R*H*F),
+ "wgrad_w13": (lambda: _run("wgrad", G, rg, off, 2*F, H, 0, dH, R, 2*F, X, H, R, 1, H, 0, gW13, H, ogs=2*F*H), 2*R*H*2*F),
+}
+tot_ms = tot_fl = 0
+for name, (fn, fl) in tests.items():
+    ms = bench(fn)
+    tot_ms += ms; tot_fl += fl
+    print(f"{name:12s} {ms:8.3f} ms  {fl/ms/1e9:8.1f} TFLOP/s")
+print(f"total {tot_ms:.3f} ms {tot_fl/tot_ms/1e9:.1f} TFLOP/s")
