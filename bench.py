@@ -1,0 +1,364 @@
+"""FSEP MoE-layer step benchmark (forward + backward) on B200.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config mixtral|fine|tiny]
+                  [--impl ours|reference] [--alpha 1.2] [--layout laer|static]
+  python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+A step = one forward + backward of the FSEP MoE layer over one batch of
+synthetic tokens per GPU (Gumbel-top-k routing with Zipf(alpha) popularity).
+`value` is whole-job tokens/s with inputs resident in HBM (device time, max over
+ranks); `e2e` is the same step through the public API with the step's inputs
+copied from pinned host memory and a result metric read back, inside the timed
+region.  Rank 0 prints one JSON line.
+
+--impl reference times the reference's CPU path on the host cores: the
+reference planner itself (oracle/_ref: plan_layout + lite_routing, 1 core) plus
+the CPU layer restatement (oracle/layer_oracle.py, numpy fp32 on all cores) on a
+bounded token sample -- the reference ships no GPU executor.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "FSEP MoE-layer fwd+bwd tokens/s at 1/2/4/8 B200, skewed routing; % roofline"
+CONFIGS = {
+    "mixtral": dict(E=8, K=2, H=4096, F=14336, T=16384,
+                    workload="Mixtral-8x7B MoE layer shape: 8 experts top-2, hidden 4096, ffn 14336, 16K tokens/GPU, bf16"),
+    "fine": dict(E=64, K=8, H=2048, F=1408, T=32768,
+                 workload="fine-grained MoE: 64 experts top-8, hidden 2048, ffn 1408, 32K tokens/GPU"),
+    "tiny": dict(E=8, K=2, H=256, F=512, T=512,
+                 workload="tiny FSEP MoE layer: 8 experts top-2, hidden 256, ffn 512, 512 tokens/device"),
+}
+SEED_DATA, SEED_PLANNER = 42, 7
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["bf16_tflops"], d["bf16_tflops_sustained"], d["hbm_gbs"], "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def default_capacity(E, K, N):
+    return E if N == 1 else max(K, min(E, 2 * E // N))
+
+
+def zipf_bias(rng, T, E, alpha, perm):
+    ranks = np.arange(1, E + 1, dtype=np.float64)
+    p = ranks ** (-alpha)
+    p /= p.sum()
+    return (np.log(p[perm])[None, :] + rng.gumbel(size=(T, E))).astype(np.float32)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.result = {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = [r.split(",") for r in out.strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for i, n in enumerate(names):
+                if len(r) > 4 + i and r[4 + i].strip().lower() == "active":
+                    reasons.add(n)
+        self.result = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                       "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU paths
+def cpu_reference_rate(cfg, N, C, alpha, sample_tokens, steps=1):
+    """Reference CPU path on a bounded sample: reference planner (oracle/_ref, 1 core)
+    + numpy fp32 layer restatement (all cores).  Returns (tokens/s, details)."""
+    from oracle import layer_oracle as LO
+    from oracle import ref as REF
+    E, K, H, F = cfg["E"], cfg["K"], cfg["H"], cfg["F"]
+    rng = np.random.default_rng(SEED_DATA)
+    bf = LO.bf16_round
+    nrm = lambda *shape: rng.standard_normal(size=shape, dtype=np.float32)
+    wg = bf(nrm(E, H) * 0.02)
+    w1 = np.stack([bf(nrm(F, H) / np.float32(np.sqrt(H))) for _ in range(E)])
+    w3 = np.stack([bf(nrm(F, H) / np.float32(np.sqrt(H))) for _ in range(E)])
+    w2 = np.stack([bf(nrm(H, F) / np.float32(np.sqrt(F))) for _ in range(E)])
+    perm = rng.permutation(E)
+    x = bf(nrm(sample_tokens, H))
+    dy = bf(nrm(sample_tokens, H) * 0.1)
+    bias = zipf_bias(rng, sample_tokens, E, alpha, perm)
+    # planner on the full-size histogram of this workload (the reference's per-layer-step call)
+    R = np.stack([np.bincount(LO.topk(zipf_bias(rng, 4096, E, alpha, perm), K)[0].reshape(-1), minlength=E)
+                  for _ in range(N)]) * (cfg["T"] // 4096 if cfg["T"] >= 4096 else 1)
+    plan_s = 0.0
+    have_ref = REF.available()
+    if have_ref and N > 1:
+        res = REF.plan_bench(R.tolist(), C, 50, bandwidth=9e11, v_comm=2.0 * H, v_comp=6.0 * H * F, b_comp=1.6354e15)
+        plan_s = (res["plan_us"] + res["route_us"]) * 1e-6
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        LO.layer_step([x], [bias], wg, w1, w3, w2, K, None, C, [dy], dtype=np.float32)
+        times.append(time.perf_counter() - t0)
+    layer_s = min(times)
+    # one layer step covers N*T tokens at the planner's cost once per step
+    per_token = layer_s / sample_tokens
+    step_s = per_token * N * cfg["T"] + plan_s
+    rate = N * cfg["T"] / step_s
+    detail = {"layer_s_per_token": per_token, "planner_us_per_step": plan_s * 1e6, "planner": "oracle/_ref"
+              if have_ref and N > 1 else "not needed at N=1 (C=E, single layout)"}
+    return rate, detail, layer_s
+
+
+def run_reference_impl(args, cfg):
+    N = args.gpus
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    C = args.capacity or default_capacity(cfg["E"], cfg["K"], N)
+    sample = args.cpu_sample or max(64, min(512, int(2.0e12 / (18 * cfg["K"] * cfg["H"] * cfg["F"]))))
+    ncores = os.cpu_count()
+    ts = []
+    rate = None
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        rate, detail, _ = cpu_reference_rate(cfg, N, C, args.alpha, sample)
+        if i >= args.warmup:
+            ts.append(time.perf_counter() - t0)
+    cpu = {"value": rate, "unit": "tokens/s", "cores": ncores, "kind": "port",
+           "sample": f"{sample} tokens/step of the {args.config} workload through oracle/layer_oracle.py "
+                     f"(numpy fp32, BLAS on {ncores} cores) + reference plan_layout+lite_routing "
+                     f"(oracle/_ref, 1 core) per layer-step; tokens/s extrapolated to {N}x{cfg['T']} tokens"}
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "tokens/s", "n_gpus": N,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": N * cfg["T"] / rate * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (Gumbel-top-k Zipf routing, random-init weights)",
+            "config": {"workload": cfg["workload"], "n_experts": cfg["E"], "top_k": cfg["K"], "hidden": cfg["H"],
+                       "ffn": cfg["F"], "tokens_per_gpu": cfg["T"], "capacity": C, "zipf_alpha": args.alpha},
+            "cpu_baseline": cpu,
+            "e2e": {"value": rate, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU path
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="mixtral", choices=list(CONFIGS))
+    ap.add_argument("--alpha", type=float, default=1.2)
+    ap.add_argument("--layout", default="laer", choices=["laer", "static"])
+    ap.add_argument("--capacity", type=int, default=0)
+    ap.add_argument("--tokens", type=int, default=0)
+    ap.add_argument("--cpu-sample", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-static", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.tokens:
+        cfg["T"] = args.tokens
+    if args.warmup < 3:
+        args.warmup = 3  # contract: at least 3 untimed warm-up steps
+    if args.impl == "reference":
+        return run_reference_impl(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    N = world
+    E, K, H, F, T = cfg["E"], cfg["K"], cfg["H"], cfg["F"], cfg["T"]
+    C = args.capacity or default_capacity(E, K, N)
+
+    from paper_2602_11686_b200 import planner as PL
+    from paper_2602_11686_b200.layer import FsepLayer, LayerSpec
+
+    layer = FsepLayer(LayerSpec(E, K, H, F, T, C, world=N, rank=rank, virtual=False))
+    if N > 1:
+        layer.connect_torch_distributed()
+    # random-init weights of the named architecture (identical on every rank)
+    g = torch.Generator(device="cuda").manual_seed(SEED_DATA)
+    for e in range(E):
+        w1 = (torch.randn(F, H, device="cuda", generator=g) / H ** 0.5).bfloat16()
+        w3 = (torch.randn(F, H, device="cuda", generator=g) / H ** 0.5).bfloat16()
+        w2 = (torch.randn(H, F, device="cuda", generator=g) / F ** 0.5).bfloat16()
+        layer.load_expert(e, w1, w3, w2)
+    layer.load_router((torch.randn(E, H, device="cuda", generator=g) * 0.02).bfloat16())
+    del w1, w3, w2
+    # synthetic data: x ~ N(0,1), dy ~ N(0, 0.1^2), per-rank seeds; Zipf routing bias from the host
+    gx = torch.Generator(device="cuda").manual_seed(SEED_DATA * 1000 + rank)
+    x = torch.randn(T, H, device="cuda", generator=gx).bfloat16()
+    dy = (torch.randn(T, H, device="cuda", generator=gx) * 0.1).bfloat16()
+    rng = np.random.default_rng(SEED_DATA + rank)
+    perm = np.random.default_rng(SEED_DATA).permutation(E)  # same popularity order on all ranks
+    n_bias = 4
+    bias_h = [torch.from_numpy(zipf_bias(rng, T, E, args.alpha, perm)).pin_memory() for _ in range(n_bias)]
+    bias_d = [b.cuda() for b in bias_h]
+    y = torch.empty_like(x)
+    dx = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+
+    cfg_json = json.dumps({"topology": {"n_nodes": 1, "devices_per_node": N, "b_intra": 9e11, "b_inter": 9e11},
+                           "cost": {"v_comm": 2.0 * H, "v_comp": 6.0 * H * F, "b_comp": peaks()[0] * 1e12},
+                           "model": {"n_experts": E, "capacity": C}, "planner": {"seed": SEED_PLANNER}})
+    if N > 1 and args.layout == "laer":
+        layer.attach_planner(PL.Config(cfg_json), layer=0)
+    elif N > 1:
+        layer.set_layout(PL.static_ep_layout(N, E, C))
+
+    def step(i):
+        layer.forward(x, bias_d[i % n_bias], T, y)
+        layer.backward(dy, dx)
+
+    def timed(nsteps, fn):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for i in range(nsteps):
+            fn(i)
+        e.record(stream)
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / nsteps
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        return ms
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    layer.stats_reset()
+    with ClockSampler(local) as clk:
+        ms = timed(args.steps, step)
+    clocks = clk.result
+    st = layer.stats()
+    value = N * T / (ms * 1e-3)
+
+    # ---- roofline of the dominant kernel class (grouped tcgen05 GEMMs)
+    burst, sustained, hbm, src = peaks()
+    gemm_tflops = st["gemm_flops"] / (st["gemm_ms"] * 1e-3) / 1e12
+    flop_tok = 18.0 * K * H * F
+    traffic = None
+    prof = ROOT / "profiles" / f"gemm_traffic_{args.config}.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": round(gemm_tflops, 1), "peak": sustained, "unit": "TFLOP/s",
+                "frac": round(gemm_tflops / sustained, 4), "traffic": traffic,
+                "kernel": "grouped tcgen05 GEMMs (6 launches/step: gate-up+SwiGLU, down, 2 dgrad, 2 wgrad)",
+                "flops_per_step": st["gemm_flops"], "gemm_ms_per_step": round(st["gemm_ms"], 4),
+                "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained ({src}); burst {burst}",
+                "frac_of_burst": round(gemm_tflops / burst, 4),
+                "step_frac": round(value / N * flop_tok / (sustained * 1e12), 4)}
+
+    # ---- static-EP comparison (same kernels, static_ep_layout at the same C)
+    static = None
+    if N > 1 and args.layout == "laer" and not args.no_static:
+        layer.detach_planner()
+        layer.set_layout(PL.static_ep_layout(N, E, C))
+        for i in range(args.warmup):
+            step(i)
+        sms = timed(args.steps, step)
+        static = {"value": N * T / (sms * 1e-3), "ms_per_step": sms, "layout": "static_ep_layout(N,E,C)"}
+
+    # ---- end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        x_h = x.cpu().pin_memory()
+        dy_h = dy.cpu().pin_memory()
+        metric_h = torch.empty(2, dtype=torch.float32).pin_memory()
+
+        def e2e_step(i):
+            x.copy_(x_h, non_blocking=True)
+            bias_d[i % n_bias].copy_(bias_h[i % n_bias], non_blocking=True)
+            dy.copy_(dy_h, non_blocking=True)
+            step(i)
+            m = torch.stack([y.float().sum(), dx.float().sum()])
+            metric_h.copy_(m, non_blocking=True)
+
+        for i in range(args.warmup):
+            e2e_step(i)
+        ems = timed(args.steps, e2e_step)
+        bi = x.numel() * 2 + dy.numel() * 2 + bias_d[0].numel() * 4
+        e2e = {"value": N * T / (ems * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": 8,
+               "ms_per_step": ems, "note": "x, dy, routing bias H2D from pinned memory + [sum y, sum dx] D2H per step"}
+
+    # ---- CPU baseline (rank 0 at N=1 only)
+    cpu = None
+    if rank == 0 and N == 1 and not args.no_cpu:
+        sample = args.cpu_sample or max(64, min(512, int(2.0e12 / (18 * K * H * F))))
+        rate, detail, secs = cpu_reference_rate(cfg, N, C, args.alpha, sample)
+        cpu = {"value": rate, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"{sample} tokens of the workload through oracle/layer_oracle.py (numpy fp32 BLAS, "
+                         f"{os.cpu_count()} cores, {secs:.1f}s); planner: {detail['planner']}; extrapolated"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": N, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic: x~N(0,1) bf16, random-init weights, Gumbel-top-k routing with Zipf popularity",
+                "config": {"workload": cfg["workload"], "n_experts": E, "top_k": K, "hidden": H, "ffn": F,
+                           "tokens_per_gpu": T, "capacity": C, "zipf_alpha": args.alpha,
+                           "layout": args.layout if N > 1 else "single device (C=E)",
+                           "parallelism": f"fsep{N}", "l2": "inputs larger than L2 (x 128 MiB + weights)"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": st["kernel_launches"] *
+                args.steps, "clocks": clocks}
+        if static:
+            line["static_ep"] = static
+        print(json.dumps(line), flush=True)
+    layer.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -148,9 +148,12 @@ mp_status mp_fsep_layer_router_grad(mp_fsep_layer* layer, uint32_t vrank, float*
 mp_status mp_fsep_layer_read(mp_fsep_layer* layer, const char* name, uint32_t vrank, void* dst, uint64_t bytes,
                              uint64_t* needed);
 
-/* Per-kernel launch count of the last forward+backward, and CUDA-event time of
- * the dominant kernel class (used by bench.py for the roofline line). */
+/* Kernel launches of the last forward+backward; mean CUDA-event time per step
+ * of the grouped-GEMM class (the dominant kernels) over the steps since
+ * mp_fsep_layer_stats_reset, and their algorithmic FLOPs per step (18*H*F per
+ * token-slot computed on this rank).  Used by bench.py's roofline line. */
 mp_status mp_fsep_layer_stats(mp_fsep_layer* layer, uint64_t* kernel_launches, double* gemm_ms, double* gemm_flops);
+mp_status mp_fsep_layer_stats_reset(mp_fsep_layer* layer);
 
 /* Capture forward+backward into a CUDA graph and replay it (bench path). */
 mp_status mp_fsep_layer_graph_step(mp_fsep_layer* layer, const void* x, const float* bias, uint32_t n_tokens,

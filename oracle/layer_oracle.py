@@ -34,10 +34,10 @@ from . import planner_port as P
 
 def bf16_round(a: np.ndarray) -> np.ndarray:
     """Round-to-nearest-even to bfloat16, returned as float32."""
-    a = np.ascontiguousarray(a, dtype=np.float32)
-    u = a.view(np.uint32).astype(np.uint64)
-    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
-    return u.astype(np.uint32).view(np.float32)
+    u = np.array(a, dtype=np.float32, copy=True).view(np.uint32)
+    u += np.uint32(0x7FFF) + ((u >> np.uint32(16)) & np.uint32(1))
+    u &= np.uint32(0xFFFF0000)
+    return u.view(np.float32)
 
 
 # ------------------------------------------------------------------- router
@@ -138,7 +138,7 @@ def _silu(g):
     return g / (1.0 + np.exp(-g))
 
 
-def layer_step(xs, biases, wg, w1, w3, w2, K: int, A: np.ndarray, C: int, dys):
+def layer_step(xs, biases, wg, w1, w3, w2, K: int, A: np.ndarray, C: int, dys, dtype=np.float64):
     """Forward + backward of the FSEP layer over N ranks.
 
     xs/dys: per-rank [T, H] (bf16 values as float32); wg [E, H]; w1/w3 [E, F, H];
@@ -154,46 +154,46 @@ def layer_step(xs, biases, wg, w1, w3, w2, K: int, A: np.ndarray, C: int, dys):
         idx_l.append(idx)
         w_l.append(w)
         logit_l.append(lg)
-    rt = route(idx_l, w_l, A, E, C)
-    f64 = np.float64
+    rt = route(idx_l, w_l, A, E, C) if A is not None else None
+    f64 = dtype  # float64 for parity checks; float32 (BLAS sgemm) for the timed CPU baseline
     ys, dxs = [], []
     dW1 = np.zeros(w1.shape, dtype=f64)
     dW3 = np.zeros(w3.shape, dtype=f64)
     dW2 = np.zeros(w2.shape, dtype=f64)
     dWg = []
     for i in range(N):
-        x = xs[i].astype(f64)
-        dy = dys[i].astype(f64)
+        x = xs[i].astype(f64, copy=False)
+        dy = dys[i].astype(f64, copy=False)
         T, H = x.shape
-        idx, w = idx_l[i], w_l[i].astype(f64)
-        y = np.zeros((T, H))
-        dx = np.zeros((T, H))
-        dw = np.zeros((T, K))
+        idx, w = idx_l[i], w_l[i].astype(f64, copy=False)
+        y = np.zeros((T, H), dtype=f64)
+        dx = np.zeros((T, H), dtype=f64)
+        dw = np.zeros((T, K), dtype=f64)
         for e in range(E):
             tk = np.argwhere(idx == e)
             if len(tk) == 0:
                 continue
             t, k = tk[:, 0], tk[:, 1]
             xe = x[t]
-            g = xe @ w1[e].astype(f64).T
-            u = xe @ w3[e].astype(f64).T
+            g = xe @ w1[e].astype(f64, copy=False).T
+            u = xe @ w3[e].astype(f64, copy=False).T
             sg = 1.0 / (1.0 + np.exp(-g))
             a = g * sg * u
-            ye = a @ w2[e].astype(f64).T
+            ye = a @ w2[e].astype(f64, copy=False).T
             y[t] += w[t, k][:, None] * ye
             dw[t, k] = np.sum(dy[t] * ye, axis=1)
             dye = w[t, k][:, None] * dy[t]
-            da = dye @ w2[e].astype(f64)
+            da = dye @ w2[e].astype(f64, copy=False)
             du = da * g * sg
             dg = da * u * sg * (1.0 + g * (1.0 - sg))
-            dx[t] += dg @ w1[e].astype(f64) + du @ w3[e].astype(f64)
+            dx[t] += dg @ w1[e].astype(f64, copy=False) + du @ w3[e].astype(f64, copy=False)
             dW2[e] += dye.T @ a
             dW1[e] += dg.T @ xe
             dW3[e] += du.T @ xe
         dl = w * (dw - np.sum(w * dw, axis=1, keepdims=True))
-        dWg_i = np.zeros((E, H))
+        dWg_i = np.zeros((E, H), dtype=f64)
         for k in range(K):
-            dx += dl[:, k:k + 1] * wg.astype(f64)[idx[:, k]]
+            dx += dl[:, k:k + 1] * wg.astype(f64, copy=False)[idx[:, k]]
             np.add.at(dWg_i, idx[:, k], dl[:, k:k + 1] * x)
         ys.append(y)
         dxs.append(dx)

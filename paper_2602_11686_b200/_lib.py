@@ -91,6 +91,7 @@ _SIGS = {
     "mp_fsep_layer_router_grad": (C.c_int, [vp, u32, vp, vp]),
     "mp_fsep_layer_read": (C.c_int, [vp, cp, u32, vp, u64, u64p]),
     "mp_fsep_layer_stats": (C.c_int, [vp, u64p, dblp, dblp]),
+    "mp_fsep_layer_stats_reset": (C.c_int, [vp]),
     "mp_fsep_layer_graph_step": (C.c_int, [vp, vp, vp, u32, vp, vp, vp, vp]),
 }
 

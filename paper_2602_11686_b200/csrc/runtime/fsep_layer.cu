@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -112,7 +113,10 @@ extern "C" struct mp_fsep_layer {
   // streams / events
   cudaStream_t side = nullptr, plan_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_restored = nullptr, ev_hist = nullptr, ev_planned = nullptr;
-  cudaEvent_t ev_g[8] = {};
+  static constexpr int kRing = 256;
+  cudaEvent_t ev_g[kRing][4] = {};  // per-step GEMM-class timing ring (fwd begin/end, bwd begin/end)
+  long long step_no = 0, stats_from = 0;
+  unsigned long long slots_sum = 0;
   int T_step = 0;
   bool restore_every_step = true;
   // graph
@@ -303,7 +307,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   barrier(L, st);
   // 5. expert FFN on the restored experts
   if (restore) CK(cudaStreamWaitEvent(st, L.ev_restored, 0));
-  CK(cudaEventRecord(L.ev_g[0], st));
+  CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][0], st));
   for (Rank& r : L.ranks) {
     GroupedGemmArgs g = gemm_args(L, r);
     g.N = 2 * F;
@@ -320,7 +324,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
     g2.ldo = H;
     launch_grouped_gemm(GemmKind::kFwdDown, r.tm_act_k, r.tm_w2_k, g2, L.num_sms, st);
   }
-  CK(cudaEventRecord(L.ev_g[1], st));
+  CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][1], st));
   barrier(L, st);
   // 6. combine
   for (size_t v = 0; v < L.ranks.size(); ++v) {
@@ -338,7 +342,7 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
                        r.dl, st);
   }
   barrier(L, st);
-  CK(cudaEventRecord(L.ev_g[2], st));
+  CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][2], st));
   for (Rank& r : L.ranks) {
     GroupedGemmArgs g = gemm_args(L, r);  // dAct -> dH (SwiGLU backward fused)
     g.N = F;
@@ -369,7 +373,7 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
     g4.out_group_stride = L.flat;
     launch_grouped_gemm(GemmKind::kBwdWgrad, r.tm_dh_mn, r.tm_x_mn, g4, L.num_sms, st);
   }
-  CK(cudaEventRecord(L.ev_g[3], st));
+  CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][3], st));
   barrier(L, st);
   for (size_t v = 0; v < L.ranks.size(); ++v) {
     Rank& r = L.ranks[v];
@@ -455,7 +459,8 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     CK(cudaStreamCreateWithFlags(&L->plan_stream, cudaStreamNonBlocking));
     for (cudaEvent_t* e : {&L->ev_fork, &L->ev_restored, &L->ev_hist, &L->ev_planned})
       CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    for (auto& e : L->ev_g) CK(cudaEventCreate(&e));
+    for (auto& ring : L->ev_g)
+      for (auto& e : ring) CK(cudaEventCreate(&e));
     CK(cudaMalloc(&L->d_peer_flags, sizeof(unsigned int*) * kMaxRanks));
     if (L->virt) {
       unsigned int* f[kMaxRanks] = {};
@@ -483,7 +488,8 @@ void mp_fsep_layer_free(mp_fsep_layer* L) {
   cudaStreamDestroy(L->side);
   cudaStreamDestroy(L->plan_stream);
   for (cudaEvent_t e : {L->ev_fork, L->ev_restored, L->ev_hist, L->ev_planned}) cudaEventDestroy(e);
-  for (auto e : L->ev_g) cudaEventDestroy(e);
+  for (auto& ring : L->ev_g)
+    for (auto e : ring) cudaEventDestroy(e);
   delete L;
 }
 
@@ -623,6 +629,7 @@ mp_status mp_fsep_layer_backward(mp_fsep_layer* L, const void* dy, void* dx, voi
     run_backward(*L, static_cast<const __nv_bfloat16*>(dy), static_cast<__nv_bfloat16*>(dx),
                  static_cast<cudaStream_t>(stream));
     L->launches_step = launches_issued() - L->launches_before;
+    ++L->step_no;
     CK(cudaGetLastError());
   });
 }
@@ -702,21 +709,38 @@ mp_status mp_fsep_layer_read(mp_fsep_layer* L, const char* name, uint32_t vrank,
 mp_status mp_fsep_layer_stats(mp_fsep_layer* L, uint64_t* kernel_launches, double* gemm_ms, double* gemm_flops) {
   return guarded([&] {
     require(L, "mp_fsep_layer_stats: NULL layer");
-    CK(cudaEventSynchronize(L->ev_g[3]));
-    float f0 = 0, f1 = 0;
-    CK(cudaEventElapsedTime(&f0, L->ev_g[0], L->ev_g[1]));
-    CK(cudaEventElapsedTime(&f1, L->ev_g[2], L->ev_g[3]));
-    if (kernel_launches) *kernel_launches = L->launches_step;
-    if (gemm_ms) *gemm_ms = static_cast<double>(f0) + static_cast<double>(f1);
-    if (gemm_flops) {
-      // algorithmic FLOPs of the grouped GEMMs this step: 18*H*F per routed token-slot (fwd 6HF + bwd 12HF)
-      unsigned long long slots = 0;
-      std::vector<unsigned long long> R(static_cast<size_t>(L->N) * L->E);
-      CK(cudaMemcpy(R.data(), L->ranks[0].R_all, R.size() * 8, cudaMemcpyDeviceToHost));
-      for (auto v : R) slots += v;
-      const double local_share = L->virt ? 1.0 : 1.0 / L->N;  // real mode: report this rank's share
-      *gemm_flops = 18.0 * L->H * L->F * static_cast<double>(slots) * local_share;
+    // Average over the steps completed since the last reset (at most the ring size).
+    const long long n = std::min<long long>(L->step_no - L->stats_from, Layer::kRing);
+    require(n > 0, "mp_fsep_layer_stats: no completed step since reset");
+    double ms = 0.0;
+    for (long long s = L->step_no - n; s < L->step_no; ++s) {
+      cudaEvent_t* ev = L->ev_g[s % Layer::kRing];
+      CK(cudaEventSynchronize(ev[3]));
+      float f0 = 0, f1 = 0;
+      CK(cudaEventElapsedTime(&f0, ev[0], ev[1]));
+      CK(cudaEventElapsedTime(&f1, ev[2], ev[3]));
+      ms += static_cast<double>(f0) + static_cast<double>(f1);
     }
+    if (kernel_launches) *kernel_launches = L->launches_step;
+    if (gemm_ms) *gemm_ms = ms / static_cast<double>(n);
+    if (gemm_flops) {
+      // algorithmic FLOPs of this rank's grouped GEMMs per step: 18*H*F per token-slot computed here
+      // (fwd 6HF + bwd 12HF), counted from the device's segment sizes of the last step
+      unsigned long long rows = 0;
+      for (Rank& r : L->ranks) {
+        std::vector<int> seg(static_cast<size_t>(L->C));
+        CK(cudaMemcpy(seg.data(), r.pt->seg_rows, seg.size() * 4, cudaMemcpyDeviceToHost));
+        for (int v : seg) rows += static_cast<unsigned long long>(v);
+      }
+      *gemm_flops = 18.0 * L->H * L->F * static_cast<double>(rows);
+    }
+  });
+}
+
+mp_status mp_fsep_layer_stats_reset(mp_fsep_layer* L) {
+  return guarded([&] {
+    require(L, "mp_fsep_layer_stats_reset: NULL layer");
+    L->stats_from = L->step_no;
   });
 }
 

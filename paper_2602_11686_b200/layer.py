@@ -104,6 +104,10 @@ class FsepLayer:
         check(self.lib.mp_fsep_layer_attach_planner(self._h, self._planner._h))
         return self._planner
 
+    def detach_planner(self) -> None:
+        check(self.lib.mp_fsep_layer_attach_planner(self._h, None))
+        self._planner = None
+
     # ------------------------------------------------------------ step
     def forward(self, x: torch.Tensor, bias: Optional[torch.Tensor], n_tokens: int, y: torch.Tensor,
                 stream=None) -> torch.Tensor:
@@ -151,6 +155,9 @@ class FsepLayer:
         ms, fl = C.c_double(), C.c_double()
         check(self.lib.mp_fsep_layer_stats(self._h, C.byref(n), C.byref(ms), C.byref(fl)))
         return {"kernel_launches": n.value, "gemm_ms": ms.value, "gemm_flops": fl.value}
+
+    def stats_reset(self) -> None:
+        check(self.lib.mp_fsep_layer_stats_reset(self._h))
 
     def close(self) -> None:
         if getattr(self, "_h", None):
