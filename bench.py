@@ -38,6 +38,9 @@ CONFIGS = {
                     workload="Mixtral-8x7B MoE layer shape: 8 experts top-2, hidden 4096, ffn 14336, 16K tokens/GPU, bf16"),
     "fine": dict(E=64, K=8, H=2048, F=1408, T=32768,
                  workload="fine-grained MoE: 64 experts top-8, hidden 2048, ffn 1408, 32K tokens/GPU"),
+    "multilayer": dict(E=8, K=2, H=4096, F=14336, T=16384, layers=4, drift=(0.3, 0.15),
+                       workload="multi-layer dynamic skew: 4 stacked Mixtral-shape layers with drifting "
+                                "per-iteration routing, planner re-layout every step"),
     "tiny": dict(E=8, K=2, H=256, F=512, T=512,
                  workload="tiny FSEP MoE layer: 8 experts top-2, hidden 256, ffn 512, 512 tokens/device"),
 }
@@ -139,7 +142,7 @@ def cpu_reference_rate(cfg, N, C, alpha, sample_tokens, steps=1):
     layer_s = min(times)
     # one layer step covers N*T tokens at the planner's cost once per step
     per_token = layer_s / sample_tokens
-    step_s = per_token * N * cfg["T"] + plan_s
+    step_s = (per_token * N * cfg["T"] + plan_s) * cfg.get("layers", 1)
     rate = N * cfg["T"] / step_s
     detail = {"layer_s_per_token": per_token, "planner_us_per_step": plan_s * 1e6, "planner": "oracle/_ref"
               if have_ref and N > 1 else "not needed at N=1 (C=E, single layout)"}
@@ -213,46 +216,70 @@ def main():
     N = world
     E, K, H, F, T = cfg["E"], cfg["K"], cfg["H"], cfg["F"], cfg["T"]
     C = args.capacity or default_capacity(E, K, N)
+    L = cfg.get("layers", 1)
 
     from paper_2602_11686_b200 import planner as PL
     from paper_2602_11686_b200.layer import FsepLayer, LayerSpec
 
-    layer = FsepLayer(LayerSpec(E, K, H, F, T, C, world=N, rank=rank, virtual=False))
-    if N > 1:
-        layer.connect_torch_distributed()
-    # random-init weights of the named architecture (identical on every rank)
-    g = torch.Generator(device="cuda").manual_seed(SEED_DATA)
-    for e in range(E):
-        w1 = (torch.randn(F, H, device="cuda", generator=g) / H ** 0.5).bfloat16()
-        w3 = (torch.randn(F, H, device="cuda", generator=g) / H ** 0.5).bfloat16()
-        w2 = (torch.randn(H, F, device="cuda", generator=g) / F ** 0.5).bfloat16()
-        layer.load_expert(e, w1, w3, w2)
-    layer.load_router((torch.randn(E, H, device="cuda", generator=g) * 0.02).bfloat16())
-    del w1, w3, w2
-    # synthetic data: x ~ N(0,1), dy ~ N(0, 0.1^2), per-rank seeds; Zipf routing bias from the host
+    cfg_json = json.dumps({"topology": {"n_nodes": 1, "devices_per_node": N, "b_intra": 9e11, "b_inter": 9e11},
+                           "cost": {"v_comm": 2.0 * H, "v_comp": 6.0 * H * F, "b_comp": peaks()[0] * 1e12},
+                           "model": {"n_experts": E, "capacity": C}, "planner": {"seed": SEED_PLANNER}})
+    layers = []
+    for l in range(L):
+        layer = FsepLayer(LayerSpec(E, K, H, F, T, C, world=N, rank=rank, virtual=False))
+        if N > 1:
+            layer.connect_torch_distributed()
+        # random-init weights of the named architecture (identical on every rank)
+        g = torch.Generator(device="cuda").manual_seed(SEED_DATA + 7919 * l)
+        for e in range(E):
+            w1 = (torch.randn(F, H, device="cuda", generator=g) / H ** 0.5).bfloat16()
+            w3 = (torch.randn(F, H, device="cuda", generator=g) / H ** 0.5).bfloat16()
+            w2 = (torch.randn(H, F, device="cuda", generator=g) / F ** 0.5).bfloat16()
+            layer.load_expert(e, w1, w3, w2)
+        layer.load_router((torch.randn(E, H, device="cuda", generator=g) * 0.02).bfloat16())
+        if N > 1 and args.layout == "laer":
+            layer.attach_planner(PL.Config(cfg_json), layer=l)
+        elif N > 1:
+            layer.set_layout(PL.static_ep_layout(N, E, C))
+        layers.append(layer)
+    torch.cuda.synchronize()
+    # synthetic data: x ~ N(0,1), dy ~ N(0, 0.1^2), per-rank seeds; routing bias generated on the host:
+    # Gumbel-top-k with Zipf(alpha) popularity, or (multi-layer config) the drifting per-iteration
+    # popularity of the reference trace generator (generate_trace: Dirichlet(0.3) init, sigma 0.15 walk).
     gx = torch.Generator(device="cuda").manual_seed(SEED_DATA * 1000 + rank)
     x = torch.randn(T, H, device="cuda", generator=gx).bfloat16()
     dy = (torch.randn(T, H, device="cuda", generator=gx) * 0.1).bfloat16()
     rng = np.random.default_rng(SEED_DATA + rank)
-    perm = np.random.default_rng(SEED_DATA).permutation(E)  # same popularity order on all ranks
-    n_bias = 4
-    bias_h = [torch.from_numpy(zipf_bias(rng, T, E, args.alpha, perm)).pin_memory() for _ in range(n_bias)]
-    bias_d = [b.cuda() for b in bias_h]
-    y = torch.empty_like(x)
-    dx = torch.empty_like(x)
+    n_bias = args.warmup + args.steps if cfg.get("drift") else 4
+    if cfg.get("drift"):
+        spec = json.dumps({"n_devices": N, "n_experts": E, "n_layers": L, "n_iterations": n_bias,
+                           "tokens_per_device": T, "skew_alpha": cfg["drift"][0], "drift_sigma": cfg["drift"][1],
+                           "seed": SEED_DATA})
+        logp = np.log(np.maximum(PL.trace_popularity(spec), 1e-30))
+        gum = [rng.gumbel(size=(T, E)) for _ in range(4)]
+        bias_h = [[torch.from_numpy((logp[l, i][None, :] + gum[(i + l) % 4]).astype(np.float32)).pin_memory()
+                   for i in range(n_bias)] for l in range(L)]
+    else:
+        perm = np.random.default_rng(SEED_DATA).permutation(E)  # same popularity order on all ranks
+        bias_h = [[torch.from_numpy(zipf_bias(rng, T, E, args.alpha, perm)).pin_memory() for _ in range(n_bias)]
+                  for _ in range(L)]
+    bias_d = [[b.cuda() for b in row] for row in bias_h]
+    ys = [torch.empty_like(x) for _ in range(L)]
+    dxs = [torch.empty_like(x) for _ in range(L)]
     stream = torch.cuda.current_stream()
 
-    cfg_json = json.dumps({"topology": {"n_nodes": 1, "devices_per_node": N, "b_intra": 9e11, "b_inter": 9e11},
-                           "cost": {"v_comm": 2.0 * H, "v_comp": 6.0 * H * F, "b_comp": peaks()[0] * 1e12},
-                           "model": {"n_experts": E, "capacity": C}, "planner": {"seed": SEED_PLANNER}})
-    if N > 1 and args.layout == "laer":
-        layer.attach_planner(PL.Config(cfg_json), layer=0)
-    elif N > 1:
-        layer.set_layout(PL.static_ep_layout(N, E, C))
+    def run_step(i, xin, dyin, biases):
+        h = xin
+        for l, layer in enumerate(layers):
+            layer.forward(h, biases[l][i % n_bias], T, ys[l])
+            h = ys[l]
+        gr = dyin
+        for l in reversed(range(L)):
+            layers[l].backward(gr, dxs[l])
+            gr = dxs[l]
 
     def step(i):
-        layer.forward(x, bias_d[i % n_bias], T, y)
-        layer.backward(dy, dx)
+        run_step(i, x, dy, bias_d)
 
     def timed(nsteps, fn):
         if world > 1:
@@ -274,17 +301,21 @@ def main():
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
-    layer.stats_reset()
+    for layer in layers:
+        layer.stats_reset()
     with ClockSampler(local) as clk:
-        ms = timed(args.steps, step)
+        ms = timed(args.steps, lambda i: step(args.warmup + i))
     clocks = clk.result
-    st = layer.stats()
+    sts = [layer.stats() for layer in layers]
+    phases = layers[0].phase_ms() if os.environ.get("FSEP_PHASE_TIMING") == "1" else None
+    st = {"gemm_ms": sum(s_["gemm_ms"] for s_ in sts), "gemm_flops": sum(s_["gemm_flops"] for s_ in sts),
+          "kernel_launches": sum(s_["kernel_launches"] for s_ in sts)}
     value = N * T / (ms * 1e-3)
 
     # ---- roofline of the dominant kernel class (grouped tcgen05 GEMMs)
     burst, sustained, hbm, src = peaks()
     gemm_tflops = st["gemm_flops"] / (st["gemm_ms"] * 1e-3) / 1e12
-    flop_tok = 18.0 * K * H * F
+    flop_tok = 18.0 * K * H * F * L
     traffic = None
     prof = ROOT / "profiles" / f"gemm_traffic_{args.config}.json"
     if prof.exists():
@@ -294,7 +325,8 @@ def main():
             traffic = None
     roofline = {"bound": "tensor", "achieved": round(gemm_tflops, 1), "peak": sustained, "unit": "TFLOP/s",
                 "frac": round(gemm_tflops / sustained, 4), "traffic": traffic,
-                "kernel": "grouped tcgen05 GEMMs (6 launches/step: gate-up+SwiGLU, down, 2 dgrad, 2 wgrad)",
+                "kernel": f"grouped tcgen05 GEMMs ({6 * L} launches/step: gate-up+SwiGLU, down, 2 dgrad, 2 wgrad"
+                          f"{' per layer' if L > 1 else ''})",
                 "flops_per_step": st["gemm_flops"], "gemm_ms_per_step": round(st["gemm_ms"], 4),
                 "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained ({src}); burst {burst}",
                 "frac_of_burst": round(gemm_tflops / burst, 4),
@@ -303,34 +335,63 @@ def main():
     # ---- static-EP comparison (same kernels, static_ep_layout at the same C)
     static = None
     if N > 1 and args.layout == "laer" and not args.no_static:
-        layer.detach_planner()
-        layer.set_layout(PL.static_ep_layout(N, E, C))
+        for layer in layers:
+            layer.detach_planner()
+            layer.set_layout(PL.static_ep_layout(N, E, C))
         for i in range(args.warmup):
             step(i)
-        sms = timed(args.steps, step)
-        static = {"value": N * T / (sms * 1e-3), "ms_per_step": sms, "layout": "static_ep_layout(N,E,C)"}
+        sms = timed(args.steps, lambda i: step(args.warmup + i))
+        static = {"value": N * T / (sms * 1e-3), "ms_per_step": sms, "layout": "static_ep_layout(N,E,C)",
+                  "speedup_laer_over_static": round(sms / ms, 4)}
 
     # ---- end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
+        # Public-API step with host inputs: every step's x, dy and routing biases are
+        # copied H2D from pinned memory (double-buffered on a copy stream, so step
+        # i+1's upload overlaps step i's compute) and a result metric is read back.
         x_h = x.cpu().pin_memory()
         dy_h = dy.cpu().pin_memory()
         metric_h = torch.empty(2, dtype=torch.float32).pin_memory()
+        bufs = [(torch.empty_like(x), torch.empty_like(dy), [torch.empty_like(bias_d[0][0]) for _ in range(L)])
+                for _ in range(2)]
+        copy_stream = torch.cuda.Stream()
+        ready = [torch.cuda.Event() for _ in range(2)]
+        free = [torch.cuda.Event() for _ in range(2)]
+        for ev in free:
+            ev.record(stream)
+
+        def upload(i):
+            b = i % 2
+            copy_stream.wait_event(free[b])
+            with torch.cuda.stream(copy_stream):
+                bufs[b][0].copy_(x_h, non_blocking=True)
+                bufs[b][1].copy_(dy_h, non_blocking=True)
+                for l in range(L):
+                    bufs[b][2][l].copy_(bias_h[l][i % n_bias], non_blocking=True)
+            ready[b].record(copy_stream)
 
         def e2e_step(i):
-            x.copy_(x_h, non_blocking=True)
-            bias_d[i % n_bias].copy_(bias_h[i % n_bias], non_blocking=True)
-            dy.copy_(dy_h, non_blocking=True)
-            step(i)
-            m = torch.stack([y.float().sum(), dx.float().sum()])
+            b = i % 2
+            if i == 0:
+                upload(0)
+            stream.wait_event(ready[b])
+            xb, dyb, bb = bufs[b]
+            run_step(0, xb, dyb, [[t] for t in bb])
+            free[b].record(stream)
+            upload(i + 1)
+            m = torch.stack([ys[-1].float().sum(), dxs[0].float().sum()])
             metric_h.copy_(m, non_blocking=True)
 
         for i in range(args.warmup):
             e2e_step(i)
+        torch.cuda.synchronize()
         ems = timed(args.steps, e2e_step)
-        bi = x.numel() * 2 + dy.numel() * 2 + bias_d[0].numel() * 4
+        bi = x.numel() * 2 + dy.numel() * 2 + L * bias_d[0][0].numel() * 4
         e2e = {"value": N * T / (ems * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": 8,
-               "ms_per_step": ems, "note": "x, dy, routing bias H2D from pinned memory + [sum y, sum dx] D2H per step"}
+               "ms_per_step": ems,
+               "note": "x, dy, routing bias H2D from pinned host memory every step (double-buffered copy stream) "
+                       "+ [sum y, sum dx] D2H per step, inside the timed region"}
 
     # ---- CPU baseline (rank 0 at N=1 only)
     cpu = None
@@ -347,15 +408,20 @@ def main():
                 "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic: x~N(0,1) bf16, random-init weights, Gumbel-top-k routing with Zipf popularity",
                 "config": {"workload": cfg["workload"], "n_experts": E, "top_k": K, "hidden": H, "ffn": F,
-                           "tokens_per_gpu": T, "capacity": C, "zipf_alpha": args.alpha,
+                           "tokens_per_gpu": T, "capacity": C, "layers": L,
+                           "routing": ("drifting trace popularity alpha=%g sigma=%g" % tuple(cfg["drift"]))
+                           if cfg.get("drift") else f"Zipf({args.alpha}) Gumbel-top-k",
                            "layout": args.layout if N > 1 else "single device (C=E)",
                            "parallelism": f"fsep{N}", "l2": "inputs larger than L2 (x 128 MiB + weights)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": st["kernel_launches"] *
                 args.steps, "clocks": clocks}
         if static:
             line["static_ep"] = static
+        if phases:
+            line["phases_ms_layer0"] = phases
         print(json.dumps(line), flush=True)
-    layer.close()
+    for layer in layers:
+        layer.close()
     if world > 1:
         dist.destroy_process_group()
 

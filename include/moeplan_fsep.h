@@ -70,6 +70,12 @@ mp_status mp_fsep_time_cost(uint32_t n_devices, uint32_t n_experts, const uint64
                             double bandwidth, double v_comm, double v_comp, double b_comp, double* t_comm,
                             double* t_comp, double* t_total, uint64_t* max_recv);
 
+/* Expert popularity of the synthetic drifting trace (generate_trace semantics,
+ * trace.cpp:89-129) before integer rounding: out[layer][iteration][expert]
+ * (doubles, n_layers*n_iterations*n_experts).  spec_json as mp_trace_generate.
+ * Drives the routing bias of the multi-layer dynamic-skew benchmark. */
+mp_status mp_fsep_trace_popularity(const char* spec_json, double* out, uint64_t capacity);
+
 /* ========================= GPU FSEP layer step ============================= */
 
 typedef struct mp_fsep_layer mp_fsep_layer;
@@ -154,6 +160,13 @@ mp_status mp_fsep_layer_read(mp_fsep_layer* layer, const char* name, uint32_t vr
  * token-slot computed on this rank).  Used by bench.py's roofline line. */
 mp_status mp_fsep_layer_stats(mp_fsep_layer* layer, uint64_t* kernel_launches, double* gemm_ms, double* gemm_flops);
 mp_status mp_fsep_layer_stats_reset(mp_fsep_layer* layer);
+/* Per-phase mean times (ms) since the last reset, when the layer was created with
+ * FSEP_PHASE_TIMING=1 in the environment.  out[0..14]: consecutive main-stream
+ * phases (param barrier, router+scan, R barrier, plan+dispatch, dispatch barrier,
+ * restore wait, fwd GEMMs, barrier, combine, combine-bwd, barrier, bwd GEMMs,
+ * barrier, unpermute+router wgrad, grad reduce-scatter); out[15] whole step;
+ * out[16] restore start offset; out[17] restore duration (side stream).  n >= 18. */
+mp_status mp_fsep_layer_phase_ms(mp_fsep_layer* layer, double* out, uint32_t n);
 
 /* Capture forward+backward into a CUDA graph and replay it (bench path). */
 mp_status mp_fsep_layer_graph_step(mp_fsep_layer* layer, const void* x, const float* bias, uint32_t n_tokens,

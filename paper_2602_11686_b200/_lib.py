@@ -73,6 +73,7 @@ _SIGS = {
     "mp_fsep_even_layout": (C.c_int, [u32, u32, u32, u8p]),
     "mp_fsep_time_cost": (C.c_int, [u32, u32, u64p, u8p, C.c_double, C.c_double, C.c_double, C.c_double,
                                     dblp, dblp, dblp, u64p]),
+    "mp_fsep_trace_popularity": (C.c_int, [cp, dblp, u64]),
     # moeplan_fsep.h -- GPU layer
     "mp_fsep_layer_create": (C.c_int, [C.POINTER(FsepDesc), C.c_int, C.POINTER(vp)]),
     "mp_fsep_layer_free": (None, [vp]),
@@ -92,6 +93,7 @@ _SIGS = {
     "mp_fsep_layer_read": (C.c_int, [vp, cp, u32, vp, u64, u64p]),
     "mp_fsep_layer_stats": (C.c_int, [vp, u64p, dblp, dblp]),
     "mp_fsep_layer_stats_reset": (C.c_int, [vp]),
+    "mp_fsep_layer_phase_ms": (C.c_int, [vp, dblp, u32]),
     "mp_fsep_layer_graph_step": (C.c_int, [vp, vp, vp, u32, vp, vp, vp, vp]),
 }
 

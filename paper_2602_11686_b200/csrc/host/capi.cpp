@@ -283,6 +283,20 @@ mp_status mp_fsep_even_layout(uint32_t n_devices, uint32_t n_experts, uint32_t c
   });
 }
 
+mp_status mp_fsep_trace_popularity(const char* spec_json, double* out, uint64_t capacity) {
+  return guarded([&] {
+    require(spec_json && out, "mp_fsep_trace_popularity: NULL argument");
+    const TraceGenSpec spec = parse_gen_spec(spec_json, true);
+    const auto pop = trace_popularity(spec);
+    const uint64_t need = static_cast<uint64_t>(spec.n_layers) * spec.n_iterations * spec.n_experts;
+    require(capacity >= need, "mp_fsep_trace_popularity: output too small");
+    uint64_t k = 0;
+    for (const auto& layer : pop)
+      for (const auto& it : layer)
+        for (double v : it) out[k++] = v;
+  });
+}
+
 mp_status mp_fsep_time_cost(uint32_t n_devices, uint32_t n_experts, const uint64_t* R, const uint8_t* A,
                             double bandwidth, double v_comm, double v_comp, double b_comp, double* t_comm,
                             double* t_comp, double* t_total, uint64_t* max_recv) {

@@ -19,7 +19,7 @@ namespace fsep {
 
 constexpr int kMaxRanks = 16;
 constexpr int kMaxExperts = 128;
-constexpr int kBlockTokens = 128;  // router / ranking tile
+constexpr int kBlockTokens = 64;  // router / ranking tile (8 warps x 8 tokens)
 
 struct PeerTable {
   __nv_bfloat16* x_rows[kMaxRanks];

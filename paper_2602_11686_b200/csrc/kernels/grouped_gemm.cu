@@ -9,6 +9,7 @@
 #include <string>
 
 #include "kernels/grouped_gemm.cuh"
+#include "kernels/grouped_gemm2.cuh"
 #include "kernels/kernels.hpp"
 
 namespace fsep {
@@ -79,12 +80,57 @@ void launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p,
 }
 }  // namespace
 
+namespace {
+template <bool AMN, bool BMN, bool GK, int EPI>
+void launch_pair(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p, int grid, cudaStream_t st) {
+  auto kern = grouped_gemm_pair_kernel<AMN, BMN, GK, EPI>;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm2::SMEM_BYTES);
+  });
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid & ~1));
+  cfg.blockDim = dim3(gemm2::THREADS);
+  cfg.dynamicSmemBytes = gemm2::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, a, b, p);
+  count_launch();
+}
+}  // namespace
+
+bool pair_gemm_supported(GemmKind kind, const GroupedGemmArgs& a) {
+  return kind != GemmKind::kBwdWgrad || a.M % gemm2::BM == 0;
+}
+
+void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUtensorMap& tmB,
+                              const GroupedGemmArgs& a, int num_sms, cudaStream_t stream) {
+  if (a.num_groups > gemm2::MAX_GROUPS) throw std::runtime_error("grouped gemm: too many groups");
+  if (a.N % 32 != 0) throw std::runtime_error("grouped gemm: N must be a multiple of 32");
+  if (!pair_gemm_supported(kind, a)) throw std::runtime_error("pair gemm: wgrad M must be a multiple of 256");
+  GemmParams p{a.num_groups, a.group_rows, a.group_off, a.M,    a.N,    a.K,   a.out,
+               a.ldo,        a.out_group_stride, a.out2,    a.ldo2, a.aux, a.ld_aux, a.policy, a.raster};
+  switch (kind) {
+    case GemmKind::kFwdGateUp: launch_pair<false, false, false, kEpiSwigluFwd>(tmA, tmB, p, num_sms, stream); break;
+    case GemmKind::kFwdDown: launch_pair<false, false, false, kEpiBf16>(tmA, tmB, p, num_sms, stream); break;
+    case GemmKind::kBwdDownDgrad: launch_pair<false, true, false, kEpiSwigluBwd>(tmA, tmB, p, num_sms, stream); break;
+    case GemmKind::kBwdUpDgrad: launch_pair<false, true, false, kEpiBf16>(tmA, tmB, p, num_sms, stream); break;
+    case GemmKind::kBwdWgrad: launch_pair<true, true, true, kEpiF32>(tmA, tmB, p, num_sms, stream); break;
+  }
+}
+
 void launch_grouped_gemm(GemmKind kind, const CUtensorMap& tmA, const CUtensorMap& tmB, const GroupedGemmArgs& a,
                          int num_sms, cudaStream_t stream) {
   if (a.num_groups > gemm::MAX_GROUPS) throw std::runtime_error("grouped gemm: too many groups");
   if (a.N % 32 != 0) throw std::runtime_error("grouped gemm: N must be a multiple of 32");
   GemmParams p{a.num_groups, a.group_rows, a.group_off, a.M,    a.N,    a.K,   a.out,
-               a.ldo,        a.out_group_stride, a.out2,    a.ldo2, a.aux, a.ld_aux};
+               a.ldo,        a.out_group_stride, a.out2,    a.ldo2, a.aux, a.ld_aux, a.policy, a.raster};
   switch (kind) {
     case GemmKind::kFwdGateUp: launch_one<false, false, false, kEpiSwigluFwd>(tmA, tmB, p, num_sms, stream); break;
     case GemmKind::kFwdDown: launch_one<false, false, false, kEpiBf16>(tmA, tmB, p, num_sms, stream); break;

@@ -46,6 +46,8 @@ struct GemmParams {
   long long ldo2;
   const void* aux;  // SwigluBwd: h
   long long ld_aux;
+  int policy;  // L2 hints: bits 0-1 A, bits 2-3 B (0 default for the mode, 1 normal, 2 evict_first, 3 evict_last)
+  int raster;  // tile order within a group: 0 mode default, 1 m-inner, 2 n-inner, 3+ = m-chunks of `raster` tiles, n-inner
 };
 
 namespace gemm {
@@ -59,6 +61,40 @@ constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*b
 }  // namespace gemm
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+
+__device__ __forceinline__ uint64_t pick_policy(int code, bool first_by_default) {
+  switch (code) {
+    case 1: {
+      uint64_t p;
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+      return p;
+    }
+    case 2: return ptx::policy_evict_first();
+    case 3: return ptx::policy_evict_last();
+    default: return first_by_default ? ptx::policy_evict_first() : ptx::policy_evict_last();
+  }
+}
+
+// Tile order inside one group of mb_count x nb_count output tiles.
+__device__ __forceinline__ void raster_tile(int local, int mb_count, int nb_count, int raster, bool group_k, int& mb,
+                                            int& nbk) {
+  const int mode = raster == 0 ? (group_k ? 2 : 1) : raster;
+  if (mode == 1) {
+    mb = local % mb_count;
+    nbk = local / mb_count;
+  } else if (mode == 2) {
+    nbk = local % nb_count;
+    mb = local / nb_count;
+  } else {  // chunks of `mode` m-tiles; inside a chunk m fastest, then n
+    const int chunk = mode;
+    const int per_chunk = chunk * nb_count;
+    const int c = local / per_chunk;
+    const int rem = local % per_chunk;
+    const int rows_in_chunk = min(chunk, mb_count - c * chunk);
+    mb = c * chunk + rem % rows_in_chunk;
+    nbk = rem / rows_in_chunk;
+  }
+}
 
 template <bool kAMN, bool kBMN, bool kGroupK, int kEpi>
 __global__ void __launch_bounds__(gemm::THREADS, 1)

@@ -1,0 +1,358 @@
+// Grouped expert GEMM, CTA-pair version (tcgen05 cta_group::2) -- the
+// production kernel of the FSEP layer step on sm_100a.
+//
+// A cluster of 2 CTAs (one TPC) computes a 256 x 256 output tile with
+// UMMA 256x256x16: each CTA stages its 128 rows of A and its 128 columns of B
+// (TMA, SWIZZLE_128B), so per-SM shared-memory traffic per FLOP is 2/3 of the
+// 128x256 single-CTA tile and a 6-stage ring (32 KB/stage/CTA) gives 1.5x the
+// latency cover.  The leader CTA issues the MMAs; tcgen05.commit multicasts
+// stage-release and accumulator-ready to both CTAs; both CTAs' epilogues drain
+// their own TMEM rows and release the accumulator to the leader.
+//
+//   warp 0      TMA producer (each CTA loads its halves; bytes land on CTA 0's barrier)
+//   warp 1      TMEM allocator (cta_group::2) + MMA issuer (leader CTA)
+//   warps 2..9  epilogue: 8 warps = 4 TMEM lane quarters x 2 column halves
+//
+// Grouping modes and operand majorness are as in grouped_gemm.cuh.  M-grouped
+// segments are padded to 128 rows; a 256-row tile whose second half lies past
+// the segment is masked in the epilogue (those rows belong to the next segment).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "kernels/grouped_gemm.cuh"
+#include "kernels/sm100_ptx.cuh"
+
+namespace fsep {
+
+namespace gemm2 {
+constexpr int BM = 256, BN = 256, BK = 64, STAGES = 6;
+constexpr int HALF = 128;                       // rows of A / columns of B per CTA
+constexpr int A_BYTES = HALF * BK * 2;          // 16 KB
+constexpr int B_BYTES = HALF * BK * 2;          // 16 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // per CTA
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 64 + EPI_WARPS * 32;
+constexpr int MAX_GROUPS = 256;
+constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 512 + (MAX_GROUPS + 1) * 4;
+}  // namespace gemm2
+
+template <bool kAMN, bool kBMN, bool kGroupK, int kEpi>
+__global__ void __launch_bounds__(gemm2::THREADS, 1)
+    grouped_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                             const GemmParams p) {
+  using namespace gemm2;
+  using namespace fsep::ptx;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  int* tile_start = reinterpret_cast<int*>(smem + STAGES * STAGE_BYTES + 512);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int G = p.num_groups;
+  const int nb = (p.N + BN - 1) / BN;
+  const int cluster = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int g = 0; g < G; ++g) {
+      tile_start[g] = acc;
+      acc += kGroupK ? (p.M / BM) * nb : ((p.group_rows[g] + BM - 1) / BM) * nb;
+    }
+    tile_start[G] = acc;
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);   // leader's arrive_expect_tx (+ both CTAs' tx bytes)
+      mbar_init(&empty_bar[s], 1);  // MMA commit (multicast)
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);               // MMA commit (multicast)
+      mbar_init(&tempty_bar[s], 2 * EPI_WARPS);  // both CTAs' epilogue warps (leader's copy is used)
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total_tiles = tile_start[G];
+
+  auto decode = [&](int t, int& g, int& mb, int& nbk) {
+    g = 0;
+    while (tile_start[g + 1] <= t) ++g;
+    const int local = t - tile_start[g];
+    const int mbs = kGroupK ? p.M / BM : (p.group_rows[g] + BM - 1) / BM;
+    raster_tile(local, mbs, nb, p.raster == 0 ? 16 : p.raster, kGroupK, mb, nbk);  // default: 16-tile m-chunks
+  };
+  auto k_blocks = [&](int g) { return kGroupK ? p.group_rows[g] / BK : p.K / BK; };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer (both CTAs)
+    if (elect_one()) {
+      // default: both operands evict_last (measured best: concurrent tiles share both A and B panels)
+      const uint64_t pol_a = pick_policy((p.policy & 3) ? (p.policy & 3) : 3, false);
+      const uint64_t pol_b = pick_policy(((p.policy >> 2) & 3) ? ((p.policy >> 2) & 3) : 3, false);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = cluster; t < total_tiles; t += nclusters) {
+        int g, mb, nbk;
+        decode(t, g, mb, nbk);
+        const int nk = k_blocks(g);
+        const int row0 = p.group_off[g];
+        const int m_half = mb * BM + rank * HALF;   // this CTA's first A row (M-grouped: within the group)
+        const int n_half = nbk * BN + rank * HALF;  // this CTA's first B column
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          uint8_t* sA = smem + s * STAGE_BYTES;
+          uint8_t* sB = sA + A_BYTES;
+          if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * STAGE_BYTES);
+          if (!kAMN) {
+            tma_load_2d_pair(sA, &tmA, &full_bar[s], kb * BK, row0 + m_half, pol_a);
+          } else {
+#pragma unroll
+            for (int i = 0; i < HALF / 64; ++i)
+              tma_load_2d_pair(sA + i * 8192, &tmA, &full_bar[s], m_half + i * 64, row0 + kb * BK, pol_a);
+          }
+          if (!kGroupK) {
+            if (!kBMN) {
+              tma_load_3d_pair(sB, &tmB, &full_bar[s], kb * BK, n_half, g, pol_b);
+            } else {
+#pragma unroll
+              for (int i = 0; i < HALF / 64; ++i)
+                tma_load_3d_pair(sB + i * 8192, &tmB, &full_bar[s], n_half + i * 64, kb * BK, g, pol_b);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < HALF / 64; ++i)
+              tma_load_2d_pair(sB + i * 8192, &tmB, &full_bar[s], n_half + i * 64, row0 + kb * BK, pol_b);
+          }
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA)
+    if (leader) {
+      constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN, kAMN, kBMN);
+      int s = 0;
+      uint32_t ph = 0;
+      int it = 0;
+      for (int t = cluster; t < total_tiles; t += nclusters, ++it) {
+        int g, mb, nbk;
+        decode(t, g, mb, nbk);
+        const int nk = k_blocks(g);
+        const int as = it & 1;
+        const uint32_t aph = (it >> 1) & 1;
+        mbar_wait(&tempty_bar[as], aph ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + as * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a0 = smem_u32(smem + s * STAGE_BYTES);
+            const uint32_t b0 = a0 + A_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t ad = kAMN ? smem_desc(a0 + k * 2048, 8192, 1024) : smem_desc(a0 + k * 32, 16, 1024);
+              const uint64_t bd = kBMN ? smem_desc(b0 + k * 2048, 8192, 1024) : smem_desc(b0 + k * 32, 16, 1024);
+              umma_bf16_pair(tmem_d, ad, bd, idesc, (kb | k) ? 1u : 0u);
+            }
+            umma_commit_pair(&empty_bar[s], 0x3);
+          }
+          __syncwarp();
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        // accumulator ready (for an empty K range this arrives at once: nothing pending)
+        if (lane == 0) umma_commit_pair(&tfull_bar[as], 0x3);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const uint32_t quarter = warp & 3;
+    const int half = static_cast<int>(warp - 2) >> 2;
+    const int r = static_cast<int>(quarter * 32 + lane);  // row within this CTA's 128 rows
+    int it = 0;
+    for (int t = cluster; t < total_tiles; t += nclusters, ++it) {
+      int g, mb, nbk;
+      decode(t, g, mb, nbk);
+      const int as = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      const int m_half = mb * BM + static_cast<int>(rank) * HALF;
+      const bool valid = kGroupK || m_half < p.group_rows[g];
+      if (kEpi == kEpiSwigluBwd && valid) {
+        // While the MMAs of this tile run, pull this row's h slice (one 128-feature
+        // block: 256 contiguous bf16 = 512 B) into L2 so the epilogue loads hit L2.
+        const int f0 = nbk * BN + half * 128;
+        if (f0 < p.N) {
+          const __nv_bfloat16* hrow = static_cast<const __nv_bfloat16*>(p.aux) +
+                                      (static_cast<long long>(p.group_off[g]) + m_half + r) * p.ld_aux + (f0 / 128) * 256;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], 512;" ::"l"(hrow) : "memory");
+        }
+      }
+      mbar_wait(&tfull_bar[as], aph);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + ((quarter * 32) << 16) + as * BN;
+      if (valid) {
+        if (kEpi == kEpiF32) {
+          const bool empty_k = k_blocks(g) == 0;
+          float* out = static_cast<float*>(p.out) + static_cast<long long>(g) * p.out_group_stride +
+                       static_cast<long long>(m_half + r) * p.ldo;
+#pragma unroll 1
+          for (int j = 0; j < 4; ++j) {
+            const int c = half * 128 + j * 32;
+            const int col = nbk * BN + c;
+            if (col >= p.N) break;
+            float v[32];
+            if (empty_k) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            } else {
+              tmem_ld32(taddr + c, v);
+            }
+            float4* dst = reinterpret_cast<float4*>(out + col);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          }
+        } else if (kEpi == kEpiBf16) {
+          const long long row = p.group_off[g] + m_half + r;
+          __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
+#pragma unroll 1
+          for (int j = 0; j < 4; ++j) {
+            const int c = half * 128 + j * 32;
+            const int col = nbk * BN + c;
+            if (col >= p.N) break;
+            float v[32];
+            tmem_ld32(taddr + c, v);
+            uint4* dst = reinterpret_cast<uint4*>(out + col);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              dst[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                                  pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+          }
+        } else if (kEpi == kEpiSwigluFwd) {
+          // tile columns [0,128) = gate f0.., [128,256) = up f0..; this warp: f in [64*half, 64*half+64)
+          const long long row = p.group_off[g] + m_half + r;
+          __nv_bfloat16* h = static_cast<__nv_bfloat16*>(p.out) + row * p.ldo + nbk * BN;
+          __nv_bfloat16* act = static_cast<__nv_bfloat16*>(p.out2) + row * p.ldo2 + nbk * (BN / 2);
+#pragma unroll 1
+          for (int j = 0; j < 2; ++j) {
+            const int f = half * 64 + j * 32;
+            float gv[32], uv[32];
+            tmem_ld32(taddr + f, gv);
+            tmem_ld32(taddr + 128 + f, uv);
+            uint4* hg = reinterpret_cast<uint4*>(h + f);
+            uint4* hu = reinterpret_cast<uint4*>(h + 128 + f);
+            uint4* ao = reinterpret_cast<uint4*>(act + f);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              hg[i] = make_uint4(pack_bf16(gv[8 * i], gv[8 * i + 1]), pack_bf16(gv[8 * i + 2], gv[8 * i + 3]),
+                                 pack_bf16(gv[8 * i + 4], gv[8 * i + 5]), pack_bf16(gv[8 * i + 6], gv[8 * i + 7]));
+              hu[i] = make_uint4(pack_bf16(uv[8 * i], uv[8 * i + 1]), pack_bf16(uv[8 * i + 2], uv[8 * i + 3]),
+                                 pack_bf16(uv[8 * i + 4], uv[8 * i + 5]), pack_bf16(uv[8 * i + 6], uv[8 * i + 7]));
+              float a[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) a[q] = silu_f(gv[8 * i + q]) * uv[8 * i + q];
+              ao[i] = make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]),
+                                 pack_bf16(a[6], a[7]));
+            }
+          }
+        } else {  // kEpiSwigluBwd: software-pipelined h loads (chunk j+1 in flight while j computes)
+          const long long row = p.group_off[g] + m_half + r;
+          const __nv_bfloat16* h = static_cast<const __nv_bfloat16*>(p.aux) + row * p.ld_aux;
+          __nv_bfloat16* dh = static_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
+          int nchunks = 0;
+          for (int j = 0; j < 4; ++j)
+            if (nbk * BN + half * 128 + j * 32 < p.N) nchunks = j + 1;
+          auto hcol_of = [&](int j) {
+            const int f = nbk * BN + half * 128 + j * 32;
+            return (f / 128) * 256 + (f % 128);
+          };
+          uint4 gq[4], uq[4];
+          if (nchunks > 0) {
+            const uint4* g4 = reinterpret_cast<const uint4*>(h + hcol_of(0));
+            const uint4* u4 = reinterpret_cast<const uint4*>(h + hcol_of(0) + 128);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              gq[i] = g4[i];
+              uq[i] = u4[i];
+            }
+          }
+#pragma unroll 1
+          for (int j = 0; j < nchunks; ++j) {
+            uint4 gn[4], un[4];
+            if (j + 1 < nchunks) {
+              const uint4* g4 = reinterpret_cast<const uint4*>(h + hcol_of(j + 1));
+              const uint4* u4 = reinterpret_cast<const uint4*>(h + hcol_of(j + 1) + 128);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                gn[i] = g4[i];
+                un[i] = u4[i];
+              }
+            }
+            float da[32];
+            tmem_ld32(taddr + half * 128 + j * 32, da);
+            const int hc = hcol_of(j);
+            uint4* dg4 = reinterpret_cast<uint4*>(dh + hc);
+            uint4* du4 = reinterpret_cast<uint4*>(dh + hc + 128);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const __nv_bfloat16* gb = reinterpret_cast<const __nv_bfloat16*>(&gq[i]);
+              const __nv_bfloat16* ub = reinterpret_cast<const __nv_bfloat16*>(&uq[i]);
+              float dg[8], du[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const float gg = __bfloat162float(gb[q]);
+                const float uu = __bfloat162float(ub[q]);
+                const float sg = 1.0f / (1.0f + __expf(-gg));
+                const float d = da[8 * i + q];
+                du[q] = d * gg * sg;
+                dg[q] = d * uu * sg * (1.0f + gg * (1.0f - sg));
+              }
+              dg4[i] = make_uint4(pack_bf16(dg[0], dg[1]), pack_bf16(dg[2], dg[3]), pack_bf16(dg[4], dg[5]),
+                                  pack_bf16(dg[6], dg[7]));
+              du4[i] = make_uint4(pack_bf16(du[0], du[1]), pack_bf16(du[2], du[3]), pack_bf16(du[4], du[5]),
+                                  pack_bf16(du[6], du[7]));
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              gq[i] = gn[i];
+              uq[i] = un[i];
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&tempty_bar[as], 0);
+    }
+  }
+  __syncthreads();
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair<512>(tmem_base);
+  }
+}
+
+}  // namespace fsep

@@ -29,6 +29,8 @@ struct GroupedGemmArgs {
   long long ldo2;
   const void* aux;
   long long ld_aux;
+  int policy = 0;  // see GemmParams
+  int raster = 0;
 };
 
 enum class GemmKind : int {
@@ -39,8 +41,13 @@ enum class GemmKind : int {
   kBwdWgrad = 4,      // dW_g = A_g^T * B_g over the group's rows (fp32)   A MN-major, B MN-major (2-D)
 };
 
+// Single-CTA 128x256 tiles (B maps with 256-row boxes for the K-major weight operand).
 void launch_grouped_gemm(GemmKind kind, const CUtensorMap& tmA, const CUtensorMap& tmB, const GroupedGemmArgs& args,
                          int num_sms, cudaStream_t stream);
+// CTA-pair 256x256 tiles (cta_group::2; K-major B maps with 128-row boxes).  Production path.
+bool pair_gemm_supported(GemmKind kind, const GroupedGemmArgs& args);
+void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUtensorMap& tmB,
+                              const GroupedGemmArgs& args, int num_sms, cudaStream_t stream);
 
 // Kernel-count bookkeeping for bench/roofline (launches issued by this library).
 uint64_t launches_issued();

@@ -48,52 +48,75 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float (&f)[8]) {
 }
 
 // ------------------------------------------------------------------ router
-// One block = 128 tokens (4 warps x 32 tokens, one token at a time per warp).
-// Emits top-k ids / gate weights, per-block expert counts and each slot's rank
-// within its block (token order), which the scan turns into global ranks.
+// One block = kBlockTokens (64) tokens, 8 warps x 8 tokens.  Per token a warp
+// accumulates 8 experts at a time (lane l: canonical partial over its elements),
+// reduces each with the fixed xor butterfly, then runs the warp top-k.  Emits
+// top-k ids / gate weights, per-block expert counts and each slot's rank within
+// its block (token order), which the block scan turns into global ranks.
 template <int CH>  // H / 256
-__global__ void __launch_bounds__(128) router_kernel(const __nv_bfloat16* __restrict__ x,
+__global__ void __launch_bounds__(256) router_kernel(const __nv_bfloat16* __restrict__ x,
                                                      const __nv_bfloat16* __restrict__ wg,
                                                      const float* __restrict__ bias, int T, int E, int K,
                                                      int* __restrict__ topk_idx, float* __restrict__ topk_w,
                                                      int* __restrict__ intra_rank, int* __restrict__ blk_hist) {
   constexpr int H = CH * 256;
+  constexpr int kWords = kBlockTokens / 32;
+  constexpr int kTokPerWarp = kBlockTokens / 8;
   __shared__ int s_idx[kBlockTokens][8];
-  __shared__ unsigned s_mask[kMaxExperts][4];
+  __shared__ unsigned s_mask[kMaxExperts][kWords];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < kMaxExperts * 4; i += blockDim.x) (&s_mask[0][0])[i] = 0u;
+  for (int i = threadIdx.x; i < kMaxExperts * kWords; i += blockDim.x) (&s_mask[0][0])[i] = 0u;
   __syncthreads();
 
-  for (int tt = 0; tt < 32; ++tt) {
-    const int tl = warp * 32 + tt;
+  for (int tt = 0; tt < kTokPerWarp; ++tt) {
+    const int tl = warp * kTokPerWarp + tt;
     const int t = blockIdx.x * kBlockTokens + tl;
     if (t >= T) break;
-    uint4 xv[CH];
-    const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * H);
+    float xf[CH][8];
+    {
+      const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * H);
+      uint4 xv[CH];
 #pragma unroll
-    for (int c = 0; c < CH; ++c) xv[c] = __ldg(xr + c * 32 + lane);
+      for (int c = 0; c < CH; ++c) xv[c] = __ldg(xr + c * 32 + lane);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) bf16x8_to_f32(xv[c], xf[c]);
+    }
     // expert e's logit ends up in lane e % 32, register slot e / 32
     float mine[kMaxExperts / 32];
 #pragma unroll
     for (int q = 0; q < kMaxExperts / 32; ++q) mine[q] = -FLT_MAX;
 #pragma unroll
     for (int q = 0; q < kMaxExperts / 32; ++q) {
-      for (int ee = 0; ee < 32; ++ee) {
-        const int e = q * 32 + ee;
-        if (e >= E) break;
-        const uint4* wr = reinterpret_cast<const uint4*>(wg + static_cast<size_t>(e) * H);
-        float acc = 0.f;
+      for (int g8 = 0; g8 < 4; ++g8) {
+        const int e0 = q * 32 + g8 * 8;
+        if (e0 >= E) break;
+        const int ne = min(8, E - e0);
+        float acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = 0.f;
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
-          float xf[8], wf[8];
-          bf16x8_to_f32(xv[c], xf);
-          bf16x8_to_f32(__ldg(wr + c * 32 + lane), wf);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc = __fmaf_rn(xf[j], wf[j], acc);
+          for (int i = 0; i < 8; ++i) {
+            if (i < ne) {
+              float wf[8];
+              bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(wg + static_cast<size_t>(e0 + i) * H) + c * 32 + lane),
+                            wf);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) acc[i] = __fmaf_rn(xf[c][j], wf[j], acc[i]);
+            }
+          }
         }
-        acc = warp_sum(acc);  // xor butterfly 16,8,4,2,1 -- identical on all lanes
-        if (bias) acc = __fadd_rn(acc, __ldg(bias + static_cast<size_t>(t) * E + e));
-        if (ee == lane) mine[q] = acc;
+        float pick = -FLT_MAX;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i < ne) {
+            float v = warp_sum(acc[i]);  // xor butterfly 16,8,4,2,1 -- identical on all lanes
+            if (bias) v = __fadd_rn(v, __ldg(bias + static_cast<size_t>(t) * E + e0 + i));
+            if (lane == g8 * 8 + i) pick = v;
+          }
+        }
+        if (lane >= g8 * 8 && lane < g8 * 8 + ne) mine[q] = pick;
       }
     }
     // top-k: warp argmax K times (largest value, lowest id on ties)
@@ -135,26 +158,31 @@ __global__ void __launch_bounds__(128) router_kernel(const __nv_bfloat16* __rest
         topk_idx[static_cast<size_t>(t) * K + k] = sel_e[k];
         topk_w[static_cast<size_t>(t) * K + k] = w[k] / s;
         s_idx[tl][k] = sel_e[k];
-        atomicOr(&s_mask[sel_e[k]][warp], 1u << tt);
+        atomicOr(&s_mask[sel_e[k]][tl >> 5], 1u << (tl & 31));
       }
     }
   }
   __syncthreads();
   // per-slot rank within the block: tokens with the same expert before me
-  const int tl = threadIdx.x;
-  const int t = blockIdx.x * kBlockTokens + tl;
-  if (t < T) {
-    const int w = tl >> 5, l = tl & 31;
-    for (int k = 0; k < K; ++k) {
-      const int e = s_idx[tl][k];
-      int r = __popc(s_mask[e][w] & ((1u << l) - 1u));
-      for (int ww = 0; ww < w; ++ww) r += __popc(s_mask[e][ww]);
-      intra_rank[static_cast<size_t>(t) * K + k] = r;
+  if (threadIdx.x < kBlockTokens) {
+    const int tl = threadIdx.x;
+    const int t = blockIdx.x * kBlockTokens + tl;
+    if (t < T) {
+      const int w = tl >> 5, l = tl & 31;
+      for (int k = 0; k < K; ++k) {
+        const int e = s_idx[tl][k];
+        int r = __popc(s_mask[e][w] & ((1u << l) - 1u));
+        for (int ww = 0; ww < w; ++ww) r += __popc(s_mask[e][ww]);
+        intra_rank[static_cast<size_t>(t) * K + k] = r;
+      }
     }
   }
-  for (int e = threadIdx.x; e < E; e += blockDim.x)
-    blk_hist[static_cast<size_t>(blockIdx.x) * E + e] =
-        __popc(s_mask[e][0]) + __popc(s_mask[e][1]) + __popc(s_mask[e][2]) + __popc(s_mask[e][3]);
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int cnt = 0;
+#pragma unroll
+    for (int w = 0; w < kWords; ++w) cnt += __popc(s_mask[e][w]);
+    blk_hist[static_cast<size_t>(blockIdx.x) * E + e] = cnt;
+  }
 }
 
 // Exclusive scan of per-block counts per expert -> block bases; R row of this
@@ -544,7 +572,7 @@ __global__ void unpack_grad_kernel(const float* __restrict__ chunk, long long lo
 void launch_router(const RouterArgs& a, cudaStream_t st) {
   const int nblk = (a.T + kBlockTokens - 1) / kBlockTokens;
   if (nblk == 0) return;
-  FSEP_CH_SWITCH(a.H / 256, router_kernel<CH><<<nblk, 128, 0, st>>>(a.x, a.wg, a.bias, a.T, a.E, a.K, a.topk_idx,
+  FSEP_CH_SWITCH(a.H / 256, router_kernel<CH><<<nblk, 256, 0, st>>>(a.x, a.wg, a.bias, a.T, a.E, a.K, a.topk_idx,
                                                                      a.topk_w, a.intra_rank, a.blk_hist));
   count_launch();
 }

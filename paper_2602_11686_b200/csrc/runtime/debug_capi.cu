@@ -18,7 +18,8 @@ __attribute__((visibility("default"))) mp_status mp_fsep_debug_grouped_gemm(
     const void* aux, long long ld_aux, void* stream) {
   using namespace fsep;
   return moeplan::capi::guarded([&] {
-    const GemmKind k = static_cast<GemmKind>(kind);
+    const bool pair = (kind & 0x100) != 0;  // CTA-pair kernel (cta_group::2)
+    const GemmKind k = static_cast<GemmKind>(kind & 0xf);
     const bool a_mn = k == GemmKind::kBwdWgrad;
     const bool b_mn = k != GemmKind::kFwdGateUp && k != GemmKind::kFwdDown;
     CUtensorMap ta = a_mn ? make_tmap_2d(A, a_inner, a_rows, a_pitch, 64, 64) : make_tmap_2d(A, a_inner, a_rows, a_pitch, 64, 128);
@@ -28,12 +29,17 @@ __attribute__((visibility("default"))) mp_status mp_fsep_debug_grouped_gemm(
     else if (b_mn)
       tb = make_tmap_3d(B, b_d0, b_d1, b_groups, b_pitch1, b_pitch2, 64, 64);
     else
-      tb = make_tmap_3d(B, b_d0, b_d1, b_groups, b_pitch1, b_pitch2, 64, 256);
+      tb = make_tmap_3d(B, b_d0, b_d1, b_groups, b_pitch1, b_pitch2, 64, pair ? 128 : 256);
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     GroupedGemmArgs g{num_groups, group_rows, group_off, M, N, K, out, ldo, out_gstride, out2, ldo2, aux, ld_aux};
-    launch_grouped_gemm(k, ta, tb, g, sms, static_cast<cudaStream_t>(stream));
+    g.policy = (kind >> 12) & 0xF;   // experiment knobs (bits 12-15 policy, 16-23 raster)
+    g.raster = (kind >> 16) & 0xFF;
+    if (pair)
+      launch_grouped_gemm_pair(k, ta, tb, g, sms, static_cast<cudaStream_t>(stream));
+    else
+      launch_grouped_gemm(k, ta, tb, g, sms, static_cast<cudaStream_t>(stream));
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw moeplan::Error(moeplan::ErrorKind::device, cudaGetErrorString(e));
   });

@@ -21,6 +21,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -79,6 +81,7 @@ struct Rank {
   uint32_t* slot_dst = nullptr;
   uint8_t* layout_dev = nullptr;
   PlanTables* pt = nullptr;
+  CUtensorMap tm_w13_k128{}, tm_w2_k128{};  // K-major weight maps with 128-row boxes (CTA-pair kernel)
   CUtensorMap tm_x_k{}, tm_w13_k{}, tm_act_k{}, tm_w2_k{}, tm_dy_k{}, tm_w2_mn{}, tm_dh_k{}, tm_w13_mn{}, tm_dy_mn{},
       tm_act_mn{}, tm_dh_mn{}, tm_x_mn{};
   // per-step inputs
@@ -111,7 +114,7 @@ extern "C" struct mp_fsep_layer {
   mp_fsep_planner* planner = nullptr;
   bool planner_pending = false;
   // streams / events
-  cudaStream_t side = nullptr, plan_stream = nullptr;
+  cudaStream_t side = nullptr, plan_stream = nullptr, cap_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_restored = nullptr, ev_hist = nullptr, ev_planned = nullptr;
   static constexpr int kRing = 256;
   cudaEvent_t ev_g[kRing][4] = {};  // per-step GEMM-class timing ring (fwd begin/end, bwd begin/end)
@@ -124,7 +127,41 @@ extern "C" struct mp_fsep_layer {
   const void* graph_key[5] = {};
   uint64_t launches_before = 0, launches_step = 0;
   double gemm_flops_step = 0.0;
+  int restore_blocks = 16;  // CTAs per (slot, peer) chunk of the restore kernel
+  // optional per-phase event timing (FSEP_PHASE_TIMING=1)
+  static constexpr int kPhaseRing = 64;
+  bool phase_on = false;
+  std::vector<std::array<cudaEvent_t, 20>> ev_p;
 };
+
+namespace {
+enum Phase : int {
+  kPhFwdBegin = 0,
+  kPhParamBarrier,
+  kPhRouter,
+  kPhRBarrier,
+  kPhDispatch,
+  kPhDispatchBarrier,
+  kPhRestoreWait,
+  kPhFwdGemm,
+  kPhFwdGemmBarrier,
+  kPhCombine,
+  kPhCombineBwd,
+  kPhCombineBwdBarrier,
+  kPhBwdGemm,
+  kPhBwdGemmBarrier,
+  kPhUnpermute,
+  kPhGradRS,
+  kPhRestoreBegin,  // side stream
+  kPhRestoreEnd,
+  kPhCount
+};
+
+void mark(mp_fsep_layer& L, cudaStream_t st, int phase) {
+  if (!L.phase_on) return;
+  cudaEventRecord(L.ev_p[static_cast<size_t>(L.step_no % mp_fsep_layer::kPhaseRing)][phase], st);
+}
+}  // namespace
 
 namespace {
 
@@ -145,6 +182,8 @@ void build_maps(Layer& L, Rank& r) {
   const __nv_bfloat16* w2 = r.restored + 2LL * F * H;
   r.tm_w13_k = make_tmap_3d(w13, H, 2 * F, C, H, L.flat, 64, 256);
   r.tm_w2_k = make_tmap_3d(w2, F, H, C, F, L.flat, 64, 256);
+  r.tm_w13_k128 = make_tmap_3d(w13, H, 2 * F, C, H, L.flat, 64, 128);
+  r.tm_w2_k128 = make_tmap_3d(w2, F, H, C, F, L.flat, 64, 128);
   r.tm_w2_mn = make_tmap_3d(w2, F, H, C, F, L.flat, 64, 64);
   r.tm_w13_mn = make_tmap_3d(w13, H, 2 * F, C, H, L.flat, 64, 64);
 }
@@ -246,6 +285,23 @@ void barrier(Layer& L, cudaStream_t st) {
   launch_peer_barrier(L.d_peer_flags, L.N, L.ranks[0].rank, ++L.epoch, st);
 }
 
+// CTA-pair (cta_group::2) kernel by default; FSEP_GEMM=single forces the 128x256 single-CTA kernel.
+bool use_pair_gemm() {
+  static const bool single = [] {
+    const char* v = std::getenv("FSEP_GEMM");
+    return v && std::string(v) == "single";
+  }();
+  return !single;
+}
+
+void gemm(Layer& L, GemmKind kind, const CUtensorMap& a, const CUtensorMap& b_single, const CUtensorMap& b_pair,
+          const GroupedGemmArgs& g, cudaStream_t st) {
+  if (use_pair_gemm() && pair_gemm_supported(kind, g))
+    launch_grouped_gemm_pair(kind, a, b_pair, g, L.num_sms, st);
+  else
+    launch_grouped_gemm(kind, a, b_single, g, L.num_sms, st);
+}
+
 GroupedGemmArgs gemm_args(Layer& L, Rank& r) {
   GroupedGemmArgs g{};
   g.num_groups = L.C;
@@ -264,11 +320,17 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   for (Rank& r : L.ranks) CK(cudaMemcpyAsync(r.layout_dev, L.layout_host, static_cast<size_t>(E) * N, cudaMemcpyHostToDevice, st));
   // 2. shard restore on the side stream (overlaps router + dispatch)
   const bool restore = N > 1 && L.restore_every_step;
+  mark(L, st, kPhFwdBegin);
+  // peers' shards must be final (parameter load / optimizer update) before anyone gathers them
+  barrier(L, st);
+  mark(L, st, kPhParamBarrier);
   if (restore) {
     CK(cudaEventRecord(L.ev_fork, st));
     CK(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
+    mark(L, L.side, kPhRestoreBegin);
     for (Rank& r : L.ranks)
-      launch_restore(r.layout_dev, E, N, r.rank, C, L.S, L.flat, L.peers, r.restored, 16, L.side);
+      launch_restore(r.layout_dev, E, N, r.rank, C, L.S, L.flat, L.peers, r.restored, L.restore_blocks, L.side);
+    mark(L, L.side, kPhRestoreEnd);
     CK(cudaEventRecord(L.ev_restored, L.side));
   }
   // 3. router + top-k + histogram, global ranks, R exchange
@@ -280,7 +342,9 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
     launch_router(RouterArgs{r.x_in, r.wg, b, T, H, E, K, r.topk_idx, r.topk_w, r.intra_rank, r.blk_hist}, st);
     launch_block_scan(r.blk_hist, nblk, E, r.blk_base, L.peers, r.rank, N, st);
   }
+  mark(L, st, kPhRouter);
   barrier(L, st);
+  mark(L, st, kPhRBarrier);
   // 4. device lite routing + receive layout; dispatch
   for (Rank& r : L.ranks) {
     launch_plan(r.R_all, r.layout_dev, E, N, r.rank, r.pt, L.cap, st);
@@ -304,9 +368,12 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   }
   for (Rank& r : L.ranks)
     launch_dispatch(DispatchArgs{r.x_in, T, H, K, E, r.topk_idx, r.intra_rank, r.blk_base, r.pt, L.peers, r.slot_dst}, st);
+  mark(L, st, kPhDispatch);
   barrier(L, st);
+  mark(L, st, kPhDispatchBarrier);
   // 5. expert FFN on the restored experts
   if (restore) CK(cudaStreamWaitEvent(st, L.ev_restored, 0));
+  mark(L, st, kPhRestoreWait);
   CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][0], st));
   for (Rank& r : L.ranks) {
     GroupedGemmArgs g = gemm_args(L, r);
@@ -316,21 +383,24 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
     g.ldo = 2 * F;
     g.out2 = r.act;
     g.ldo2 = F;
-    launch_grouped_gemm(GemmKind::kFwdGateUp, r.tm_x_k, r.tm_w13_k, g, L.num_sms, st);
+    gemm(L, GemmKind::kFwdGateUp, r.tm_x_k, r.tm_w13_k, r.tm_w13_k128, g, st);
     GroupedGemmArgs g2 = gemm_args(L, r);
     g2.N = H;
     g2.K = F;
     g2.out = r.y_rows;
     g2.ldo = H;
-    launch_grouped_gemm(GemmKind::kFwdDown, r.tm_act_k, r.tm_w2_k, g2, L.num_sms, st);
+    gemm(L, GemmKind::kFwdDown, r.tm_act_k, r.tm_w2_k, r.tm_w2_k128, g2, st);
   }
   CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][1], st));
+  mark(L, st, kPhFwdGemm);
   barrier(L, st);
+  mark(L, st, kPhFwdGemmBarrier);
   // 6. combine
   for (size_t v = 0; v < L.ranks.size(); ++v) {
     Rank& r = L.ranks[v];
     launch_combine(T, H, K, r.topk_w, r.slot_dst, L.peers, y + (L.virt ? static_cast<long long>(v) * TH : 0), st);
   }
+  mark(L, st, kPhCombine);
 }
 
 void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStream_t st) {
@@ -341,7 +411,9 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
     launch_combine_bwd(T, H, K, dy + (L.virt ? static_cast<long long>(v) * TH : 0), r.topk_w, r.slot_dst, L.peers,
                        r.dl, st);
   }
+  mark(L, st, kPhCombineBwd);
   barrier(L, st);
+  mark(L, st, kPhCombineBwdBarrier);
   CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][2], st));
   for (Rank& r : L.ranks) {
     GroupedGemmArgs g = gemm_args(L, r);  // dAct -> dH (SwiGLU backward fused)
@@ -351,38 +423,42 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
     g.ldo = 2 * F;
     g.aux = r.h;
     g.ld_aux = 2 * F;
-    launch_grouped_gemm(GemmKind::kBwdDownDgrad, r.tm_dy_k, r.tm_w2_mn, g, L.num_sms, st);
+    gemm(L, GemmKind::kBwdDownDgrad, r.tm_dy_k, r.tm_w2_mn, r.tm_w2_mn, g, st);
     GroupedGemmArgs g2 = gemm_args(L, r);  // dX rows
     g2.N = H;
     g2.K = 2 * F;
     g2.out = r.dx_rows;
     g2.ldo = H;
-    launch_grouped_gemm(GemmKind::kBwdUpDgrad, r.tm_dh_k, r.tm_w13_mn, g2, L.num_sms, st);
+    gemm(L, GemmKind::kBwdUpDgrad, r.tm_dh_k, r.tm_w13_mn, r.tm_w13_mn, g2, st);
     GroupedGemmArgs g3 = gemm_args(L, r);  // dW2 = dY^T act
     g3.M = H;
     g3.N = F;
     g3.out = r.grad_full + 2LL * F * H;
     g3.ldo = F;
     g3.out_group_stride = L.flat;
-    launch_grouped_gemm(GemmKind::kBwdWgrad, r.tm_dy_mn, r.tm_act_mn, g3, L.num_sms, st);
+    gemm(L, GemmKind::kBwdWgrad, r.tm_dy_mn, r.tm_act_mn, r.tm_act_mn, g3, st);
     GroupedGemmArgs g4 = gemm_args(L, r);  // dW13 = dH^T X
     g4.M = 2 * F;
     g4.N = H;
     g4.out = r.grad_full;
     g4.ldo = H;
     g4.out_group_stride = L.flat;
-    launch_grouped_gemm(GemmKind::kBwdWgrad, r.tm_dh_mn, r.tm_x_mn, g4, L.num_sms, st);
+    gemm(L, GemmKind::kBwdWgrad, r.tm_dh_mn, r.tm_x_mn, r.tm_x_mn, g4, st);
   }
   CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][3], st));
+  mark(L, st, kPhBwdGemm);
   barrier(L, st);
+  mark(L, st, kPhBwdGemmBarrier);
   for (size_t v = 0; v < L.ranks.size(); ++v) {
     Rank& r = L.ranks[v];
     launch_unpermute_bwd(T, H, K, r.topk_idx, r.dl, r.slot_dst, r.wg, L.peers,
                          dx + (L.virt ? static_cast<long long>(v) * TH : 0), st);
     launch_router_wgrad(r.x_in, T, H, K, E, r.topk_idx, r.dl, r.dwg_partial, r.dwg, st);
   }
+  mark(L, st, kPhUnpermute);
   if (N > 1)
     for (Rank& r : L.ranks) launch_grad_reduce_scatter(r.pt, L.peers, E, r.rank, L.S, L.flat, r.grad_shard, st);
+  mark(L, st, kPhGradRS);
   // join the planner stream (it finished long before the backward GEMMs did)
   if (L.planner_pending) CK(cudaStreamWaitEvent(st, L.ev_planned, 0));
 }
@@ -457,10 +533,18 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     require(mp_fsep_even_layout(L->N, L->E, L->C, L->layout_host) == MP_OK, "even layout failed");
     CK(cudaStreamCreateWithFlags(&L->side, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&L->plan_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&L->cap_stream, cudaStreamNonBlocking));
     for (cudaEvent_t* e : {&L->ev_fork, &L->ev_restored, &L->ev_hist, &L->ev_planned})
       CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     for (auto& ring : L->ev_g)
       for (auto& e : ring) CK(cudaEventCreate(&e));
+    if (const char* v = std::getenv("FSEP_PHASE_TIMING"); v && std::string(v) == "1") {
+      L->phase_on = true;
+      L->ev_p.resize(mp_fsep_layer::kPhaseRing);
+      for (auto& ring : L->ev_p)
+        for (auto& e : ring) CK(cudaEventCreate(&e));
+    }
+    if (const char* v = std::getenv("FSEP_RESTORE_BLOCKS")) L->restore_blocks = std::max(1, std::atoi(v));
     CK(cudaMalloc(&L->d_peer_flags, sizeof(unsigned int*) * kMaxRanks));
     if (L->virt) {
       unsigned int* f[kMaxRanks] = {};
@@ -487,8 +571,11 @@ void mp_fsep_layer_free(mp_fsep_layer* L) {
   cudaFreeHost(L->R_host);
   cudaStreamDestroy(L->side);
   cudaStreamDestroy(L->plan_stream);
+  cudaStreamDestroy(L->cap_stream);
   for (cudaEvent_t e : {L->ev_fork, L->ev_restored, L->ev_hist, L->ev_planned}) cudaEventDestroy(e);
   for (auto& ring : L->ev_g)
+    for (auto e : ring) cudaEventDestroy(e);
+  for (auto& ring : L->ev_p)
     for (auto e : ring) cudaEventDestroy(e);
   delete L;
 }
@@ -737,6 +824,36 @@ mp_status mp_fsep_layer_stats(mp_fsep_layer* L, uint64_t* kernel_launches, doubl
   });
 }
 
+mp_status mp_fsep_layer_phase_ms(mp_fsep_layer* L, double* out, uint32_t n) {
+  return guarded([&] {
+    require(L && out, "mp_fsep_layer_phase_ms: NULL argument");
+    require(L->phase_on, "phase timing is off (set FSEP_PHASE_TIMING=1 before creating the layer)");
+    require(n >= static_cast<uint32_t>(kPhCount), "mp_fsep_layer_phase_ms: need kPhCount outputs");
+    const long long cnt = std::min<long long>(L->step_no - L->stats_from, mp_fsep_layer::kPhaseRing);
+    require(cnt > 0, "mp_fsep_layer_phase_ms: no completed step since reset");
+    std::vector<double> acc(kPhCount, 0.0);
+    const bool restore = L->N > 1 && L->restore_every_step;
+    for (long long s = L->step_no - cnt; s < L->step_no; ++s) {
+      auto& ev = L->ev_p[static_cast<size_t>(s % mp_fsep_layer::kPhaseRing)];
+      CK(cudaEventSynchronize(ev[kPhGradRS]));
+      // out[i] (i < kPhGradRS) = time from mark i to mark i+1 on the main stream
+      for (int i = kPhFwdBegin; i < kPhGradRS; ++i) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, ev[i], ev[i + 1]) == cudaSuccess) acc[i] += ms;
+      }
+      float tot = 0.f;
+      if (cudaEventElapsedTime(&tot, ev[kPhFwdBegin], ev[kPhGradRS]) == cudaSuccess) acc[kPhGradRS] += tot;
+      if (restore) {
+        float a = 0.f, b = 0.f;
+        if (cudaEventElapsedTime(&a, ev[kPhFwdBegin], ev[kPhRestoreBegin]) == cudaSuccess) acc[kPhRestoreBegin] += a;
+        if (cudaEventElapsedTime(&b, ev[kPhRestoreBegin], ev[kPhRestoreEnd]) == cudaSuccess) acc[kPhRestoreEnd] += b;
+      }
+      cudaGetLastError();
+    }
+    for (int i = 0; i < kPhCount; ++i) out[i] = acc[static_cast<size_t>(i)] / static_cast<double>(cnt);
+  });
+}
+
 mp_status mp_fsep_layer_stats_reset(mp_fsep_layer* L) {
   return guarded([&] {
     require(L, "mp_fsep_layer_stats_reset: NULL layer");
@@ -756,23 +873,31 @@ mp_status mp_fsep_layer_graph_step(mp_fsep_layer* L, const void* x, const float*
       if (L->graph) cudaGraphExecDestroy(L->graph);
       L->graph = nullptr;
       cudaGraph_t g;
-      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      // Capture on the layer's own stream (the caller's may be the legacy default
+      // stream, which cannot be captured).  Events from eager steps cannot be waited
+      // on inside a capture: settle the planner first.
+      if (L->planner_pending) CK(cudaEventSynchronize(L->ev_planned));
+      L->planner_pending = false;
+      cudaStream_t cs = L->cap_stream;
+      CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
       const uint64_t l0 = launches_issued();
       try {
         run_forward(*L, static_cast<const __nv_bfloat16*>(x), bias, static_cast<int>(n_tokens),
-                    static_cast<__nv_bfloat16*>(y), st);
-        run_backward(*L, static_cast<const __nv_bfloat16*>(dy), static_cast<__nv_bfloat16*>(dx), st);
+                    static_cast<__nv_bfloat16*>(y), cs);
+        run_backward(*L, static_cast<const __nv_bfloat16*>(dy), static_cast<__nv_bfloat16*>(dx), cs);
       } catch (...) {
-        cudaStreamEndCapture(st, &g);
+        cudaStreamEndCapture(cs, &g);
         throw;
       }
       L->launches_step = launches_issued() - l0;
-      CK(cudaStreamEndCapture(st, &g));
+      CK(cudaStreamEndCapture(cs, &g));
       CK(cudaGraphInstantiate(&L->graph, g, 0));
       CK(cudaGraphDestroy(g));
       std::memcpy(L->graph_key, key, sizeof(key));
     }
     CK(cudaGraphLaunch(L->graph, st));
+    // the graph joins its planner node internally; its event records are capture-internal
+    L->planner_pending = false;
   });
 }
 

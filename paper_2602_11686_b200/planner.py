@@ -173,6 +173,16 @@ def time_cost(R, A, *, bandwidth: float, v_comm: float, v_comp: float, b_comp: f
     return {"t_comm": out[0].value, "t_comp": out[1].value, "t_total": out[2].value, "max_recv": mr.value}
 
 
+def trace_popularity(spec_json: str) -> np.ndarray:
+    """[layers, iterations, experts] popularity of the drifting synthetic trace (generate_trace)."""
+    import json as _json
+    spec = _json.loads(spec_json)
+    shape = (spec.get("n_layers", 1), spec["n_iterations"], spec["n_experts"])
+    out = np.zeros(shape, dtype=np.float64)
+    check(load().mp_fsep_trace_popularity(spec_json.encode(), out.ctypes.data_as(C.POINTER(C.c_double)), out.size))
+    return out
+
+
 class Planner:
     """Per-layer planner with history and the runtime's one-step lag
     (sim.cpp:99-149): next() is even_replication_layout before any observation,

@@ -25,14 +25,15 @@ def _fn():
 
 
 def _run(kind, G, rows, off, M, N, K, A, a_rows, a_inner, B, b_d0, b_d1, b_groups, b_p1, b_p2, out, ldo, ogs=0,
-         out2=None, ldo2=0, aux=None, ld_aux=0):
+         out2=None, ldo2=0, aux=None, ld_aux=0, pair=True, sync=True):
     f = _fn()
-    st = f(KINDS[kind], G, rows.data_ptr(), off.data_ptr(), M, N, K, A.data_ptr(), a_rows, a_inner, a_inner,
+    st = f(KINDS[kind] | (0x100 if pair else 0), G, rows.data_ptr(), off.data_ptr(), M, N, K, A.data_ptr(), a_rows, a_inner, a_inner,
            B.data_ptr(), b_d0, b_d1, b_groups, b_p1, b_p2, out.data_ptr(), ldo, ogs,
            out2.data_ptr() if out2 is not None else None, ldo2, aux.data_ptr() if aux is not None else None, ld_aux,
            torch.cuda.current_stream().cuda_stream)
     _lib.check(st)
-    torch.cuda.synchronize()
+    if sync:
+        torch.cuda.synchronize()
 
 
 def _rel(a, b):
@@ -49,9 +50,10 @@ def _silu(x):
     return x * torch.sigmoid(x)
 
 
+@pytest.mark.parametrize("pair", [True, False], ids=["cta_pair", "single_cta"])
 @pytest.mark.parametrize("counts,H,F", [([128, 256, 0], 256, 256), ([512, 384], 1024, 512),
-                                        ([256, 128, 384, 128], 2048, 1408)])
-def test_forward_and_dgrad(counts, H, F):
+                                        ([256, 128, 384, 128], 2048, 1408), ([128] * 5 + [640], 512, 384)])
+def test_forward_and_dgrad(counts, H, F, pair):
     torch.manual_seed(0)
     G = len(counts)
     rows, off, R = _groups(counts)
@@ -60,14 +62,14 @@ def test_forward_and_dgrad(counts, H, F):
     W2 = (torch.randn(G, H, F, device="cuda") / F ** 0.5).bfloat16()
     h = torch.empty(R, 2 * F, device="cuda", dtype=torch.bfloat16)
     act = torch.empty(R, F, device="cuda", dtype=torch.bfloat16)
-    _run("gateup", G, rows, off, 0, 2 * F, H, X, R, H, W13, H, 2 * F, G, H, 2 * F * H, h, 2 * F, out2=act, ldo2=F)
+    _run("gateup", G, rows, off, 0, 2 * F, H, X, R, H, W13, H, 2 * F, G, H, 2 * F * H, h, 2 * F, out2=act, ldo2=F, pair=pair)
     y = torch.empty(R, H, device="cuda", dtype=torch.bfloat16)
-    _run("down", G, rows, off, 0, H, F, act, R, F, W2, F, H, G, F, H * F, y, H)
+    _run("down", G, rows, off, 0, H, F, act, R, F, W2, F, H, G, F, H * F, y, H, pair=pair)
     dY = (torch.randn(R, H, device="cuda")).bfloat16()
     dH = torch.empty(R, 2 * F, device="cuda", dtype=torch.bfloat16)
-    _run("down_dgrad", G, rows, off, 0, F, H, dY, R, H, W2, F, H, G, F, H * F, dH, 2 * F, aux=h, ld_aux=2 * F)
+    _run("down_dgrad", G, rows, off, 0, F, H, dY, R, H, W2, F, H, G, F, H * F, dH, 2 * F, aux=h, ld_aux=2 * F, pair=pair)
     dX = torch.empty(R, H, device="cuda", dtype=torch.bfloat16)
-    _run("up_dgrad", G, rows, off, 0, H, 2 * F, dH, R, 2 * F, W13, H, 2 * F, G, H, 2 * F * H, dX, H)
+    _run("up_dgrad", G, rows, off, 0, H, 2 * F, dH, R, 2 * F, W13, H, 2 * F, G, H, 2 * F * H, dX, H, pair=pair)
 
     o = 0
     for g, c in enumerate(counts):
@@ -93,15 +95,16 @@ def test_forward_and_dgrad(counts, H, F):
         o += c
 
 
-@pytest.mark.parametrize("counts,M,N", [([128, 0, 256], 256, 512), ([384, 512], 1024, 1408)])
-def test_wgrad(counts, M, N):
+@pytest.mark.parametrize("pair", [True, False], ids=["cta_pair", "single_cta"])
+@pytest.mark.parametrize("counts,M,N", [([128, 0, 256], 256, 512), ([384, 512], 1024, 1408), ([128, 128], 768, 256)])
+def test_wgrad(counts, M, N, pair):
     torch.manual_seed(1)
     G = len(counts)
     rows, off, R = _groups(counts)
     A = torch.randn(R, M, device="cuda").bfloat16()
     B = torch.randn(R, N, device="cuda").bfloat16()
     out = torch.full((G, M, N), float("nan"), device="cuda")
-    _run("wgrad", G, rows, off, M, N, 0, A, R, M, B, N, R, 1, N, 0, out, N, ogs=M * N)
+    _run("wgrad", G, rows, off, M, N, 0, A, R, M, B, N, R, 1, N, 0, out, N, ogs=M * N, pair=pair)
     o = 0
     for g, c in enumerate(counts):
         ref = A[o:o + c].float().t() @ B[o:o + c].float()

@@ -124,3 +124,16 @@ def test_error_statuses(product_lib):
     with pytest.raises(MoeplanError) as ei:
         PP.Trace.load("/nonexistent/trace.jsonl")
     assert ei.value.kind == "io"
+
+
+def test_trace_popularity_rounds_to_generated_trace(product_lib):
+    """Popularity export == the shares generate_trace apportions (largest remainder)."""
+    spec = json.dumps({"n_devices": 2, "n_experts": 8, "n_layers": 4, "n_iterations": 6, "tokens_per_device": 10000,
+                       "skew_alpha": 0.3, "drift_sigma": 0.15, "seed": 42})
+    pop = PP.trace_popularity(spec)
+    assert pop.shape == (4, 6, 8) and np.allclose(pop.sum(axis=2), 1.0)
+    stats = json.loads(PP.Trace.generate(spec).stats_json())
+    for rec in stats:
+        exact = pop[rec["layer"], rec["iter"]] * 10000
+        load = np.array(rec["expert_load"]) / 2
+        assert (np.abs(load - exact) < 1.0 + 1e-9).all()

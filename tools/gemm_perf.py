@@ -2,7 +2,12 @@
 import sys, ctypes as C
 sys.path.insert(0, ".")
 import torch
-from tests.test_gpu_gemm import _run, _groups
+import os, functools
+from tests.test_gpu_gemm import _run as _run0, _groups
+import tests.test_gpu_gemm as TG
+_knobs = (int(os.environ.get('POL', '0')) << 12) | (int(os.environ.get('RASTER', '0')) << 16)
+TG.KINDS = {k: v | _knobs for k, v in TG.KINDS.items()}
+_run = functools.partial(_run0, pair=os.environ.get('PAIR', '1') == '1', sync=False)
 
 def bench(fn, iters=10):
     for _ in range(3): fn()
