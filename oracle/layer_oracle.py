@@ -12,9 +12,8 @@ layout A (planner), lite routing S (planner.cpp:238-287) -- via
 oracle/planner_port.py, itself pinned against the reference library.
 
 Bit-exact parts (must match the GPU exactly):
-  * router logits in the canonical order the kernel uses (lane l of 32 owns
-    elements 256c + 8l + j; sequential fp32 accumulation over (c, j); fixed
-    xor-butterfly 16/8/4/2/1; + bias) -- products of two bf16 values are exact
+  * router logits in the canonical order the kernel uses (one sequential fp32
+    accumulation over h, then + bias) -- products of two bf16 values are exact
     in fp32, so FMA on the GPU equals multiply-then-add here;
   * top-k (largest logit, lowest expert id on ties), R, S, every token-slot's
     destination (device, row) and the per-device segment layout.
@@ -42,23 +41,18 @@ def bf16_round(a: np.ndarray) -> np.ndarray:
 
 # ------------------------------------------------------------------- router
 def router_logits(x: np.ndarray, wg: np.ndarray, bias: np.ndarray | None) -> np.ndarray:
-    """Canonical-order fp32 logits [T, E] (see module docstring)."""
+    """Canonical-order fp32 logits [T, E]: one sequential fp32 accumulation over
+    h (products of bf16 values are exact in fp32, so this equals the kernel's
+    FMA chain in csrc/kernels/router.cu), then + bias."""
     T, H = x.shape
-    E = wg.shape[0]
-    ch = H // 256
-    xv = x.astype(np.float32).reshape(T, ch, 32, 8)
-    wv = wg.astype(np.float32).reshape(E, ch, 32, 8)
-    acc = np.zeros((T, E, 32), dtype=np.float32)
-    for c in range(ch):
-        for j in range(8):
-            acc = acc + xv[:, None, c, :, j] * wv[None, :, c, :, j]
-    while acc.shape[-1] > 1:
-        half = acc.shape[-1] // 2
-        acc = acc[..., :half] + acc[..., half:]
-    logits = acc[..., 0]
+    xv = np.ascontiguousarray(x.astype(np.float32).T)    # [H, T]
+    wv = np.ascontiguousarray(wg.astype(np.float32).T)   # [H, E]
+    acc = np.zeros((T, wg.shape[0]), dtype=np.float32)
+    for h in range(H):
+        acc += xv[h][:, None] * wv[h][None, :]
     if bias is not None:
-        logits = logits + bias.astype(np.float32)
-    return logits
+        acc = acc + bias.astype(np.float32)
+    return acc
 
 
 def topk(logits: np.ndarray, k: int):

@@ -1,0 +1,328 @@
+// Router of the FSEP layer step: logits = x . wg^T (+ bias), top-k (ties to the
+// lowest expert id), softmax over the selected k, per-block expert histograms and
+// in-block slot ranks (token order).  CUDA cores, register-tiled.
+//
+// Canonical fp32 order (the bit-exactness contract with oracle/layer_oracle.py):
+//   logit[t][e] = fma(x[t][H-1], w[e][H-1], ... fma(x[t][1], w[e][1], fma(x[t][0], w[e][0], 0)) ...) + bias[t][e]
+// i.e. one sequential fp32 accumulation over h.  Both operands are bf16, so each
+// product is exact in fp32 and the FMA equals multiply-then-add; only the adds
+// round, in a fixed order.  Tensor cores are not used here on purpose: their
+// accumulation order is not specified, and routing must be reproducible bit for
+// bit on the CPU.
+//
+// Block = kBlockTokens (64) tokens x all E experts.  The hidden dimension is
+// streamed in 64-wide chunks staged (bf16 -> fp32, transposed h-major) in shared
+// memory; each thread owns a TT x TE (tokens x experts) register tile.
+#include <cuda_bf16.h>
+
+#include <cfloat>
+#include <stdexcept>
+
+#include "kernels/fsep_types.cuh"
+#include "kernels/kernels.hpp"
+#include "kernels/routing.hpp"
+
+namespace fsep {
+namespace {
+
+constexpr int kHC = 64;  // hidden chunk
+
+template <int TT, int TE>
+__global__ void __launch_bounds__(512) router_gemm_kernel(const __nv_bfloat16* __restrict__ x,
+                                                          const __nv_bfloat16* __restrict__ wg,
+                                                          const float* __restrict__ bias, int T, int H, int E, int K,
+                                                          int* __restrict__ topk_idx, float* __restrict__ topk_w,
+                                                          int* __restrict__ intra_rank, int* __restrict__ blk_hist) {
+  constexpr int BT = kBlockTokens;
+  constexpr int kWords = BT / 32;
+  extern __shared__ float smem[];
+  float* s_x = smem;                // [kHC][BT]    h-major
+  float* s_w = smem + kHC * BT;     // [kHC][E]     h-major
+  float* s_logit = smem;            // [BT][E + 1]  (reuses the staging area afterwards)
+  __shared__ int s_idx[BT][8];
+  __shared__ unsigned s_mask[kMaxExperts][kWords];
+
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int t0 = blockIdx.x * BT;
+  const int egroups = E / TE;
+  const int tg = tid / egroups, eg = tid % egroups;  // this thread's tile
+  for (int i = tid; i < kMaxExperts * kWords; i += nthr) (&s_mask[0][0])[i] = 0u;
+
+  float acc[TT][TE];
+#pragma unroll
+  for (int i = 0; i < TT; ++i)
+#pragma unroll
+    for (int j = 0; j < TE; ++j) acc[i][j] = 0.f;
+
+  // staging work items: x = BT tokens x 8 sixteen-byte pieces; w = E x 8 pieces
+  const int x_items = BT * (kHC / 8), w_items = E * (kHC / 8);
+  for (int h0 = 0; h0 < H; h0 += kHC) {
+    __syncthreads();
+    for (int it = tid; it < x_items; it += nthr) {
+      const int tt = it % BT, piece = it / BT;
+      const int t = min(t0 + tt, T - 1);  // clamp: rows past T are never selected
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * H + h0) + piece);
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(b[k]);
+        s_x[(piece * 8 + 2 * k) * BT + tt] = f.x;
+        s_x[(piece * 8 + 2 * k + 1) * BT + tt] = f.y;
+      }
+    }
+    for (int it = tid; it < w_items; it += nthr) {
+      const int e = it % E, piece = it / E;
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(wg + static_cast<size_t>(e) * H + h0) + piece);
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(b[k]);
+        s_w[(piece * 8 + 2 * k) * E + e] = f.x;
+        s_w[(piece * 8 + 2 * k + 1) * E + e] = f.y;
+      }
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int h = 0; h < kHC; ++h) {
+      float xv[TT], wv[TE];
+      if constexpr (TT == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(s_x + h * BT + tg * TT);
+        xv[0] = v.x, xv[1] = v.y, xv[2] = v.z, xv[3] = v.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < TT; ++i) xv[i] = s_x[h * BT + tg * TT + i];
+      }
+      if constexpr (TE == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(s_w + h * E + eg * TE);
+        wv[0] = v.x, wv[1] = v.y, wv[2] = v.z, wv[3] = v.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < TE; ++j) wv[j] = s_w[h * E + eg * TE + j];
+      }
+#pragma unroll
+      for (int i = 0; i < TT; ++i)
+#pragma unroll
+        for (int j = 0; j < TE; ++j) acc[i][j] = __fmaf_rn(xv[i], wv[j], acc[i][j]);
+    }
+  }
+  __syncthreads();
+  // logits (+ bias) -> shared memory
+#pragma unroll
+  for (int i = 0; i < TT; ++i) {
+    const int tt = tg * TT + i;
+    const int t = t0 + tt;
+#pragma unroll
+    for (int j = 0; j < TE; ++j) {
+      const int e = eg * TE + j;
+      float v = acc[i][j];
+      if (bias && t < T) v = __fadd_rn(v, __ldg(bias + static_cast<size_t>(t) * E + e));
+      s_logit[tt * (E + 1) + e] = v;
+    }
+  }
+  __syncthreads();
+  // top-k per token: a warp per token (largest logit, lowest id on ties)
+  const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
+  for (int tt = warp; tt < BT; tt += nwarps) {
+    const int t = t0 + tt;
+    if (t >= T) break;
+    float mine[kMaxExperts / 32];
+#pragma unroll
+    for (int q = 0; q < kMaxExperts / 32; ++q) {
+      const int e = q * 32 + lane;
+      mine[q] = e < E ? s_logit[tt * (E + 1) + e] : -FLT_MAX;
+    }
+    float sel_v[8];
+    int sel_e[8];
+    for (int k = 0; k < K; ++k) {
+      float bv = -FLT_MAX;
+      int be = 0x7fffffff;
+#pragma unroll
+      for (int q = 0; q < kMaxExperts / 32; ++q) {
+        const int e = q * 32 + lane;
+        if (e < E && (mine[q] > bv || (mine[q] == bv && e < be))) {
+          bv = mine[q];
+          be = e;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+        if (ov > bv || (ov == bv && oe < be)) {
+          bv = ov;
+          be = oe;
+        }
+      }
+      sel_v[k] = bv;
+      sel_e[k] = be;
+#pragma unroll
+      for (int q = 0; q < kMaxExperts / 32; ++q)  // exclude the winner (below -FLT_MAX)
+        if (q == (be >> 5) && (be & 31) == lane) mine[q] = -INFINITY;
+    }
+    if (lane == 0) {
+      float w[8], s = 0.f;
+      for (int k = 0; k < K; ++k) {
+        w[k] = expf(sel_v[k] - sel_v[0]);
+        s += w[k];
+      }
+      for (int k = 0; k < K; ++k) {
+        topk_idx[static_cast<size_t>(t) * K + k] = sel_e[k];
+        topk_w[static_cast<size_t>(t) * K + k] = w[k] / s;
+        s_idx[tt][k] = sel_e[k];
+        atomicOr(&s_mask[sel_e[k]][tt >> 5], 1u << (tt & 31));
+      }
+    }
+  }
+  __syncthreads();
+  // per-slot rank within the block (tokens with the same expert before me) + counts
+  for (int tt = tid; tt < BT; tt += nthr) {
+    const int t = t0 + tt;
+    if (t >= T) break;
+    const int w = tt >> 5, l = tt & 31;
+    for (int k = 0; k < K; ++k) {
+      const int e = s_idx[tt][k];
+      int r = __popc(s_mask[e][w] & ((1u << l) - 1u));
+      for (int ww = 0; ww < w; ++ww) r += __popc(s_mask[e][ww]);
+      intra_rank[static_cast<size_t>(t) * K + k] = r;
+    }
+  }
+  for (int e = tid; e < E; e += nthr) {
+    int cnt = 0;
+#pragma unroll
+    for (int w = 0; w < kWords; ++w) cnt += __popc(s_mask[e][w]);
+    blk_hist[static_cast<size_t>(blockIdx.x) * E + e] = cnt;
+  }
+}
+
+// Small-E variant (E <= 16): one thread per token holds all E accumulators and
+// streams its token row from HBM in 16-byte pieces; expert-weight pieces are the
+// same for every thread of the warp (broadcast loads, L1-resident).  Same
+// canonical order: per (token, expert) one FMA chain over h ascending.
+template <int E_>
+__global__ void __launch_bounds__(kBlockTokens) router_small_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg, const float* __restrict__ bias, int T,
+    int H, int K, int* __restrict__ topk_idx, float* __restrict__ topk_w, int* __restrict__ intra_rank,
+    int* __restrict__ blk_hist) {
+  constexpr int BT = kBlockTokens;
+  constexpr int kWords = BT / 32;
+  __shared__ int s_idx[BT][8];
+  __shared__ unsigned s_mask[E_][kWords];
+  const int tt = threadIdx.x;
+  const int t = blockIdx.x * BT + tt;
+  for (int i = tt; i < E_ * kWords; i += BT) (&s_mask[0][0])[i] = 0u;
+  __syncthreads();
+  if (t < T) {
+    float acc[E_];
+#pragma unroll
+    for (int e = 0; e < E_; ++e) acc[e] = 0.f;
+    const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * H);
+    const uint4* wr = reinterpret_cast<const uint4*>(wg);
+    const int pieces = H / 8;
+#pragma unroll 2
+    for (int p = 0; p < pieces; ++p) {
+      float xf[8];
+      {
+        const uint4 q = __ldg(xr + p);
+        const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __bfloat1622float2(b[k]);
+          xf[2 * k] = f.x;
+          xf[2 * k + 1] = f.y;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < E_; ++e) {
+        const uint4 q = __ldg(wr + static_cast<size_t>(e) * pieces + p);
+        const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __bfloat1622float2(b[k]);
+          acc[e] = __fmaf_rn(xf[2 * k], f.x, acc[e]);
+          acc[e] = __fmaf_rn(xf[2 * k + 1], f.y, acc[e]);
+        }
+      }
+    }
+    if (bias) {
+#pragma unroll
+      for (int e = 0; e < E_; ++e) acc[e] = __fadd_rn(acc[e], __ldg(bias + static_cast<size_t>(t) * E_ + e));
+    }
+    // top-k: largest logit, lowest id on ties (strict > in ascending e)
+    unsigned taken = 0u;
+    float sel_v[8];
+    int sel_e[8];
+    for (int k = 0; k < K; ++k) {
+      float bv = -INFINITY;
+      int be = -1;
+#pragma unroll
+      for (int e = 0; e < E_; ++e)
+        if (!(taken >> e & 1u) && (be < 0 || acc[e] > bv)) {
+          bv = acc[e];
+          be = e;
+        }
+      taken |= 1u << be;
+      sel_v[k] = bv;
+      sel_e[k] = be;
+    }
+    float w[8], s = 0.f;
+    for (int k = 0; k < K; ++k) {
+      w[k] = expf(sel_v[k] - sel_v[0]);
+      s += w[k];
+    }
+    for (int k = 0; k < K; ++k) {
+      topk_idx[static_cast<size_t>(t) * K + k] = sel_e[k];
+      topk_w[static_cast<size_t>(t) * K + k] = w[k] / s;
+      s_idx[tt][k] = sel_e[k];
+      atomicOr(&s_mask[sel_e[k]][tt >> 5], 1u << (tt & 31));
+    }
+  }
+  __syncthreads();
+  if (t < T) {
+    const int w = tt >> 5, l = tt & 31;
+    for (int k = 0; k < K; ++k) {
+      const int e = s_idx[tt][k];
+      int r = __popc(s_mask[e][w] & ((1u << l) - 1u));
+      for (int ww = 0; ww < w; ++ww) r += __popc(s_mask[e][ww]);
+      intra_rank[static_cast<size_t>(t) * K + k] = r;
+    }
+  }
+  for (int e = tt; e < E_; e += BT) {
+    int cnt = 0;
+#pragma unroll
+    for (int w = 0; w < kWords; ++w) cnt += __popc(s_mask[e][w]);
+    blk_hist[static_cast<size_t>(blockIdx.x) * E_ + e] = cnt;
+  }
+}
+
+template <int TT, int TE>
+void launch_tiled(const RouterArgs& a, int nblk, cudaStream_t st) {
+  const int threads = (kBlockTokens / TT) * (a.E / TE);
+  const size_t smem = static_cast<size_t>(kHC) * (kBlockTokens + a.E) * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(router_gemm_kernel<TT, TE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    attr = true;
+  }
+  router_gemm_kernel<TT, TE><<<nblk, threads, smem, st>>>(a.x, a.wg, a.bias, a.T, a.H, a.E, a.K, a.topk_idx,
+                                                          a.topk_w, a.intra_rank, a.blk_hist);
+}
+
+}  // namespace
+
+void launch_router(const RouterArgs& a, cudaStream_t st) {
+  const int nblk = (a.T + kBlockTokens - 1) / kBlockTokens;
+  if (nblk == 0) return;
+  if (a.E % 8 != 0 || a.E > kMaxExperts) throw std::runtime_error("router: n_experts must be a multiple of 8, <= 128");
+  if (a.H % kHC != 0) throw std::runtime_error("router: hidden must be a multiple of 64");
+  if (a.E == 8)
+    router_small_kernel<8><<<nblk, kBlockTokens, 0, st>>>(a.x, a.wg, a.bias, a.T, a.H, a.K, a.topk_idx, a.topk_w,
+                                                         a.intra_rank, a.blk_hist);
+  else if (a.E == 16)
+    router_small_kernel<16><<<nblk, kBlockTokens, 0, st>>>(a.x, a.wg, a.bias, a.T, a.H, a.K, a.topk_idx, a.topk_w,
+                                                          a.intra_rank, a.blk_hist);
+  else
+    launch_tiled<4, 4>(a, nblk, st);  // 16 x E/4 threads, register-tiled
+  count_launch();
+}
+
+}  // namespace fsep

@@ -1,15 +1,12 @@
-// Router, ranking, lite-routing assignment, dispatch/combine and their
-// backward passes for the FSEP layer step (sm_100a, CUDA cores; all of these
-// are HBM/NVLink-bound byte movers or tiny integer work).
+// Ranking, lite-routing assignment, dispatch/combine and their backward passes
+// for the FSEP layer step (sm_100a, CUDA cores; all of these are HBM/NVLink-bound
+// byte movers or tiny integer work).  The router itself is in router.cu.
 //
 // Bit-exactness contract with the CPU oracle (oracle/layer_oracle.py):
-//  * router logits use a canonical fp32 order: lane l of a warp accumulates
-//    x[256c + 8l + j] * wg[e, 256c + 8l + j] over (c, j) in order with FMA
-//    (exact products: both operands are bf16), then a fixed xor butterfly
-//    16,8,4,2,1; the per-token fp32 bias is added last;
-//  * top-k picks the largest logit, ties to the lowest expert id;
 //  * token ranks within (source, expert) follow ascending token index, and the
-//    replica split reproduces lite_routing (planner.cpp:277-282).
+//    replica split reproduces lite_routing (planner.cpp:277-282);
+//  * every token-slot's destination (device, row) and the per-device segment
+//    layout are integer functions of R, the layout and the ranks.
 #include <cuda_bf16.h>
 
 #include <cfloat>
@@ -45,144 +42,6 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float (&f)[8]) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
   return q;
-}
-
-// ------------------------------------------------------------------ router
-// One block = kBlockTokens (64) tokens, 8 warps x 8 tokens.  Per token a warp
-// accumulates 8 experts at a time (lane l: canonical partial over its elements),
-// reduces each with the fixed xor butterfly, then runs the warp top-k.  Emits
-// top-k ids / gate weights, per-block expert counts and each slot's rank within
-// its block (token order), which the block scan turns into global ranks.
-template <int CH>  // H / 256
-__global__ void __launch_bounds__(256) router_kernel(const __nv_bfloat16* __restrict__ x,
-                                                     const __nv_bfloat16* __restrict__ wg,
-                                                     const float* __restrict__ bias, int T, int E, int K,
-                                                     int* __restrict__ topk_idx, float* __restrict__ topk_w,
-                                                     int* __restrict__ intra_rank, int* __restrict__ blk_hist) {
-  constexpr int H = CH * 256;
-  constexpr int kWords = kBlockTokens / 32;
-  constexpr int kTokPerWarp = kBlockTokens / 8;
-  __shared__ int s_idx[kBlockTokens][8];
-  __shared__ unsigned s_mask[kMaxExperts][kWords];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < kMaxExperts * kWords; i += blockDim.x) (&s_mask[0][0])[i] = 0u;
-  __syncthreads();
-
-  for (int tt = 0; tt < kTokPerWarp; ++tt) {
-    const int tl = warp * kTokPerWarp + tt;
-    const int t = blockIdx.x * kBlockTokens + tl;
-    if (t >= T) break;
-    float xf[CH][8];
-    {
-      const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * H);
-      uint4 xv[CH];
-#pragma unroll
-      for (int c = 0; c < CH; ++c) xv[c] = __ldg(xr + c * 32 + lane);
-#pragma unroll
-      for (int c = 0; c < CH; ++c) bf16x8_to_f32(xv[c], xf[c]);
-    }
-    // expert e's logit ends up in lane e % 32, register slot e / 32
-    float mine[kMaxExperts / 32];
-#pragma unroll
-    for (int q = 0; q < kMaxExperts / 32; ++q) mine[q] = -FLT_MAX;
-#pragma unroll
-    for (int q = 0; q < kMaxExperts / 32; ++q) {
-      for (int g8 = 0; g8 < 4; ++g8) {
-        const int e0 = q * 32 + g8 * 8;
-        if (e0 >= E) break;
-        const int ne = min(8, E - e0);
-        float acc[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (i < ne) {
-              float wf[8];
-              bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(wg + static_cast<size_t>(e0 + i) * H) + c * 32 + lane),
-                            wf);
-#pragma unroll
-              for (int j = 0; j < 8; ++j) acc[i] = __fmaf_rn(xf[c][j], wf[j], acc[i]);
-            }
-          }
-        }
-        float pick = -FLT_MAX;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (i < ne) {
-            float v = warp_sum(acc[i]);  // xor butterfly 16,8,4,2,1 -- identical on all lanes
-            if (bias) v = __fadd_rn(v, __ldg(bias + static_cast<size_t>(t) * E + e0 + i));
-            if (lane == g8 * 8 + i) pick = v;
-          }
-        }
-        if (lane >= g8 * 8 && lane < g8 * 8 + ne) mine[q] = pick;
-      }
-    }
-    // top-k: warp argmax K times (largest value, lowest id on ties)
-    float sel_v[8];
-    int sel_e[8];
-    for (int k = 0; k < K; ++k) {
-      float bv = -FLT_MAX;
-      int be = 0x7fffffff;
-#pragma unroll
-      for (int q = 0; q < kMaxExperts / 32; ++q) {
-        const int e = q * 32 + lane;
-        if (e < E && (mine[q] > bv || (mine[q] == bv && e < be))) {
-          bv = mine[q];
-          be = e;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oe = __shfl_xor_sync(0xffffffffu, be, o);
-        if (ov > bv || (ov == bv && oe < be)) {
-          bv = ov;
-          be = oe;
-        }
-      }
-      sel_v[k] = bv;
-      sel_e[k] = be;
-#pragma unroll
-      for (int q = 0; q < kMaxExperts / 32; ++q)  // exclude the winner (below -FLT_MAX)
-        if (q == (be >> 5) && (be & 31) == lane) mine[q] = -INFINITY;
-    }
-    if (lane == 0) {
-      float w[8], s = 0.f;
-      for (int k = 0; k < K; ++k) {
-        w[k] = expf(sel_v[k] - sel_v[0]);
-        s += w[k];
-      }
-      for (int k = 0; k < K; ++k) {
-        topk_idx[static_cast<size_t>(t) * K + k] = sel_e[k];
-        topk_w[static_cast<size_t>(t) * K + k] = w[k] / s;
-        s_idx[tl][k] = sel_e[k];
-        atomicOr(&s_mask[sel_e[k]][tl >> 5], 1u << (tl & 31));
-      }
-    }
-  }
-  __syncthreads();
-  // per-slot rank within the block: tokens with the same expert before me
-  if (threadIdx.x < kBlockTokens) {
-    const int tl = threadIdx.x;
-    const int t = blockIdx.x * kBlockTokens + tl;
-    if (t < T) {
-      const int w = tl >> 5, l = tl & 31;
-      for (int k = 0; k < K; ++k) {
-        const int e = s_idx[tl][k];
-        int r = __popc(s_mask[e][w] & ((1u << l) - 1u));
-        for (int ww = 0; ww < w; ++ww) r += __popc(s_mask[e][ww]);
-        intra_rank[static_cast<size_t>(t) * K + k] = r;
-      }
-    }
-  }
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int cnt = 0;
-#pragma unroll
-    for (int w = 0; w < kWords; ++w) cnt += __popc(s_mask[e][w]);
-    blk_hist[static_cast<size_t>(blockIdx.x) * E + e] = cnt;
-  }
 }
 
 // Exclusive scan of per-block counts per expert -> block bases; R row of this
@@ -366,12 +225,24 @@ __global__ void __launch_bounds__(256) combine_kernel(int T, int K, const float*
 // dy[slot(t,k)] = w[t,k] * dout[t]   (scattered back to the expert's device)
 // dw[t,k]       = <dout[t], y[slot(t,k)]>
 // dl[t,k]       = w_k (dw_k - sum_j w_j dw_j)       (softmax-over-top-k backward)
+// Also scatters dl into the dense bf16 matrix dL[t][e] (kDLCols wide, pre-zeroed)
+// that feeds the router weight-gradient GEMM, and (block 0) writes that GEMM's
+// split-K group table: groups of kRouterWgradChunk token rows.
 template <int CH>
 __global__ void __launch_bounds__(256) combine_bwd_kernel(int T, int K, const __nv_bfloat16* __restrict__ dout,
                                                           const float* __restrict__ topk_w,
+                                                          const int* __restrict__ topk_idx,
                                                           const uint32_t* __restrict__ slot_dst, PeerTable peers,
-                                                          float* __restrict__ dl) {
+                                                          float* __restrict__ dl, __nv_bfloat16* __restrict__ dl_dense,
+                                                          int* __restrict__ rw_rows, int* __restrict__ rw_off) {
   constexpr int H = CH * 256;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const int tpad = (T + 127) / 128 * 128;
+    for (int g = 0, r = 0; r < tpad; ++g, r += kRouterWgradChunk) {
+      rw_off[g] = r;
+      rw_rows[g] = min(kRouterWgradChunk, tpad - r);
+    }
+  }
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -417,7 +288,11 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(int T, int K, const __
     mix += w[k] * dw[k];
   }
   if (lane == 0)
-    for (int k = 0; k < K; ++k) dl[static_cast<size_t>(t) * K + k] = w[k] * (dw[k] - mix);
+    for (int k = 0; k < K; ++k) {
+      const float v = w[k] * (dw[k] - mix);
+      dl[static_cast<size_t>(t) * K + k] = v;
+      dl_dense[static_cast<size_t>(t) * kDLCols + topk_idx[static_cast<size_t>(t) * K + k]] = __float2bfloat16_rn(v);
+    }
 }
 
 // ----------------------------------------------------------- unpermute bwd
@@ -461,34 +336,15 @@ __global__ void __launch_bounds__(256) unpermute_bwd_kernel(int T, int K, const 
 }
 
 // ------------------------------------------------------------ router wgrad
-// partial[split][e][col] = sum over the split's tokens of dl[t,k] * x[t,col]
-// for e = topk_idx[t,k]; reduced over splits in fixed order by the second kernel.
-__global__ void __launch_bounds__(256) router_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ x, int T, int H,
-                                                                   int K, int E, const int* __restrict__ topk_idx,
-                                                                   const float* __restrict__ dl, int tokens_per_split,
-                                                                   float* __restrict__ partial) {
-  extern __shared__ float s_acc[];  // [E][256]
-  const int col = blockIdx.x * 256 + threadIdx.x;
-  for (int e = 0; e < E; ++e) s_acc[e * 256 + threadIdx.x] = 0.f;
-  const int t0 = blockIdx.y * tokens_per_split;
-  const int t1 = min(T, t0 + tokens_per_split);
-  for (int t = t0; t < t1; ++t) {
-    const float xv = __bfloat162float(x[static_cast<size_t>(t) * H + col]);
-    for (int k = 0; k < K; ++k) {
-      const int e = topk_idx[static_cast<size_t>(t) * K + k];
-      s_acc[e * 256 + threadIdx.x] += dl[static_cast<size_t>(t) * K + k] * xv;
-    }
-  }
-  for (int e = 0; e < E; ++e)
-    partial[(static_cast<size_t>(blockIdx.y) * E + e) * H + col] = s_acc[e * 256 + threadIdx.x];
-}
-
-__global__ void router_wgrad_reduce_kernel(const float* __restrict__ partial, int splits, int EH,
+// dWg = dL^T x runs as a split-K tcgen05 GEMM (K-grouped over token chunks, one
+// [kDLCols x H] fp32 partial per chunk); the partials' first E rows are summed
+// here in fixed chunk order (deterministic).
+__global__ void router_wgrad_reduce_kernel(const float* __restrict__ partial, int splits, int EH, int H,
                                            float* __restrict__ dwg) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= EH) return;
   float s = 0.f;
-  for (int p = 0; p < splits; ++p) s += partial[static_cast<size_t>(p) * EH + i];
+  for (int p = 0; p < splits; ++p) s += partial[static_cast<size_t>(p) * kDLCols * H + i];
   dwg[i] = s;
 }
 
@@ -507,16 +363,32 @@ __global__ void grad_reduce_scatter_kernel(const PlanTables* __restrict__ pt, Pe
                                              static_cast<long long>(rank) * S);
   }
   float4* dst = reinterpret_cast<float4*>(grad_shard + static_cast<long long>(e) * S);
-  for (long long i = blockIdx.x * blockDim.x + threadIdx.x; i < S / 4; i += gridDim.x * blockDim.x) {
-    float4 a = src[0][i];
+  // 4 elements per thread per round, all replicas' loads issued before the sums
+  // (peer loads are ~2 us away); summation order stays ascending-device.
+  constexpr int U = 4;
+  const long long n = S / 4;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    float4 a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * stride < n) a[u] = src[0][i0 + u * stride];
     for (int h = 1; h < nh; ++h) {
-      const float4 b = src[h][i];
-      a.x += b.x;
-      a.y += b.y;
-      a.z += b.z;
-      a.w += b.w;
+      float4 b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i0 + u * stride < n) b[u] = src[h][i0 + u * stride];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        a[u].x += b[u].x;
+        a[u].y += b[u].y;
+        a[u].z += b[u].z;
+        a[u].w += b[u].w;
+      }
     }
-    dst[i] = a;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * stride < n) dst[i0 + u * stride] = a[u];
   }
 }
 
@@ -569,14 +441,6 @@ __global__ void unpack_grad_kernel(const float* __restrict__ chunk, long long lo
     default: throw std::runtime_error("hidden size must be 256 * {1,2,4,8,16}");         \
   }
 
-void launch_router(const RouterArgs& a, cudaStream_t st) {
-  const int nblk = (a.T + kBlockTokens - 1) / kBlockTokens;
-  if (nblk == 0) return;
-  FSEP_CH_SWITCH(a.H / 256, router_kernel<CH><<<nblk, 256, 0, st>>>(a.x, a.wg, a.bias, a.T, a.E, a.K, a.topk_idx,
-                                                                     a.topk_w, a.intra_rank, a.blk_hist));
-  count_launch();
-}
-
 void launch_block_scan(const int* blk_hist, int nblk, int E, int* blk_base, const PeerTable& peers, int rank,
                        int world, cudaStream_t st) {
   block_scan_kernel<<<1, 128, 0, st>>>(blk_hist, nblk, E, blk_base, peers, rank, world);
@@ -609,11 +473,14 @@ void launch_combine(int T, int H, int K, const float* topk_w, const uint32_t* sl
   count_launch();
 }
 
-void launch_combine_bwd(int T, int H, int K, const __nv_bfloat16* dout, const float* topk_w, const uint32_t* slot_dst,
-                        const PeerTable& peers, float* dl, cudaStream_t st) {
+void launch_combine_bwd(int T, int H, int K, const __nv_bfloat16* dout, const float* topk_w, const int* topk_idx,
+                        const uint32_t* slot_dst, const PeerTable& peers, float* dl, __nv_bfloat16* dl_dense,
+                        int* rw_rows, int* rw_off, cudaStream_t st) {
   if (T == 0) return;
-  FSEP_CH_SWITCH(H / 256,
-                 combine_bwd_kernel<CH><<<(T + 7) / 8, 256, 0, st>>>(T, K, dout, topk_w, slot_dst, peers, dl));
+  const size_t tpad = (static_cast<size_t>(T) + 127) / 128 * 128;
+  cudaMemsetAsync(dl_dense, 0, tpad * kDLCols * sizeof(__nv_bfloat16), st);
+  FSEP_CH_SWITCH(H / 256, combine_bwd_kernel<CH><<<(T + 7) / 8, 256, 0, st>>>(T, K, dout, topk_w, topk_idx, slot_dst,
+                                                                               peers, dl, dl_dense, rw_rows, rw_off));
   count_launch();
 }
 
@@ -625,20 +492,35 @@ void launch_unpermute_bwd(int T, int H, int K, const int* topk_idx, const float*
   count_launch();
 }
 
-int router_wgrad_splits(int T) { return T == 0 ? 1 : (T + 255) / 256; }
+int router_wgrad_splits(int T) {
+  const int tpad = (T + 127) / 128 * 128;
+  return tpad == 0 ? 1 : (tpad + kRouterWgradChunk - 1) / kRouterWgradChunk;
+}
 
-void launch_router_wgrad(const __nv_bfloat16* x, int T, int H, int K, int E, const int* topk_idx, const float* dl,
-                         float* partial, float* dwg, cudaStream_t st) {
+void launch_router_wgrad(const __nv_bfloat16* x, int T, int H, int E, const __nv_bfloat16* dl_dense, int T_max,
+                         const int* rw_rows, const int* rw_off, float* partial, float* dwg, int num_sms,
+                         cudaStream_t st) {
   const int splits = router_wgrad_splits(T);
-  const size_t smem = static_cast<size_t>(E) * 256 * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(router_wgrad_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
-    attr = true;
+  if (T > 0) {
+    // dL [rows][kDLCols] and x [rows][H] are both MN-major operands of the K-grouped GEMM
+    const uint64_t tmax_pad = (static_cast<uint64_t>(T_max) + 127) / 128 * 128;
+    const CUtensorMap ta = make_tmap_2d(dl_dense, kDLCols, tmax_pad, kDLCols, 64, 64);
+    const CUtensorMap tb = make_tmap_2d(x, H, static_cast<uint64_t>(T), H, 64, 64);
+    GroupedGemmArgs g{};
+    g.num_groups = splits;
+    g.group_rows = rw_rows;
+    g.group_off = rw_off;
+    g.M = kDLCols;
+    g.N = H;
+    g.out = partial;
+    g.ldo = H;
+    g.out_group_stride = static_cast<long long>(kDLCols) * H;
+    launch_grouped_gemm(GemmKind::kBwdWgrad, ta, tb, g, num_sms, st);
+  } else {
+    cudaMemsetAsync(partial, 0, static_cast<size_t>(kDLCols) * H * sizeof(float), st);
   }
-  router_wgrad_partial_kernel<<<dim3(H / 256, splits), 256, smem, st>>>(x, T, H, K, E, topk_idx, dl, 256, partial);
-  router_wgrad_reduce_kernel<<<(E * H + 255) / 256, 256, 0, st>>>(partial, splits, E * H, dwg);
-  count_launch(2);
+  router_wgrad_reduce_kernel<<<(E * H + 255) / 256, 256, 0, st>>>(partial, splits, E * H, H, dwg);
+  count_launch();
 }
 
 void launch_grad_reduce_scatter(const PlanTables* pt, const PeerTable& peers, int E, int rank, long long S,

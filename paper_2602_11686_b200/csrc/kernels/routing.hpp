@@ -41,13 +41,15 @@ void launch_zero_pad(const PlanTables* pt, int C, int H, __nv_bfloat16* x_rows, 
 void launch_dispatch(const DispatchArgs& a, cudaStream_t st);
 void launch_combine(int T, int H, int K, const float* topk_w, const uint32_t* slot_dst, const PeerTable& peers,
                     __nv_bfloat16* out, cudaStream_t st);
-void launch_combine_bwd(int T, int H, int K, const __nv_bfloat16* dout, const float* topk_w, const uint32_t* slot_dst,
-                        const PeerTable& peers, float* dl, cudaStream_t st);
+void launch_combine_bwd(int T, int H, int K, const __nv_bfloat16* dout, const float* topk_w, const int* topk_idx,
+                        const uint32_t* slot_dst, const PeerTable& peers, float* dl, __nv_bfloat16* dl_dense,
+                        int* rw_rows, int* rw_off, cudaStream_t st);
 void launch_unpermute_bwd(int T, int H, int K, const int* topk_idx, const float* dl, const uint32_t* slot_dst,
                           const __nv_bfloat16* wg, const PeerTable& peers, __nv_bfloat16* dx, cudaStream_t st);
 int router_wgrad_splits(int T);
-void launch_router_wgrad(const __nv_bfloat16* x, int T, int H, int K, int E, const int* topk_idx, const float* dl,
-                         float* partial, float* dwg, cudaStream_t st);
+void launch_router_wgrad(const __nv_bfloat16* x, int T, int H, int E, const __nv_bfloat16* dl_dense, int T_max,
+                         const int* rw_rows, const int* rw_off, float* partial, float* dwg, int num_sms,
+                         cudaStream_t st);
 void launch_grad_reduce_scatter(const PlanTables* pt, const PeerTable& peers, int E, int rank, long long S,
                                 long long flat, float* grad_shard, cudaStream_t st);
 void launch_pack_expert(const __nv_bfloat16* w1, const __nv_bfloat16* w3, const __nv_bfloat16* w2, int H, int F,

@@ -76,6 +76,8 @@ struct Rank {
   __nv_bfloat16 *h = nullptr, *act = nullptr, *dh = nullptr;
   __nv_bfloat16* wg = nullptr;
   float *dwg = nullptr, *dwg_partial = nullptr;
+  __nv_bfloat16* dl_dense = nullptr;  // [T_max pad][kDLCols] router-gradient scatter
+  int *rw_rows = nullptr, *rw_off = nullptr;
   int *topk_idx = nullptr, *intra_rank = nullptr, *blk_hist = nullptr, *blk_base = nullptr;
   float *topk_w = nullptr, *dl = nullptr;
   uint32_t* slot_dst = nullptr;
@@ -127,7 +129,7 @@ extern "C" struct mp_fsep_layer {
   const void* graph_key[5] = {};
   uint64_t launches_before = 0, launches_step = 0;
   double gemm_flops_step = 0.0;
-  int restore_blocks = 16;  // CTAs per (slot, peer) chunk of the restore kernel
+  int restore_blocks = 32;  // CTAs per (slot, peer) chunk of the restore kernel
   // optional per-phase event timing (FSEP_PHASE_TIMING=1)
   static constexpr int kPhaseRing = 64;
   bool phase_on = false;
@@ -230,7 +232,9 @@ void allocate_rank(Layer& L, Rank& r) {
   accp(cap * 2 * F * 2);  // dh
   accp(E * H * 2);        // wg
   accp(E * H * 4);        // dwg
-  accp(static_cast<size_t>(splits) * E * H * 4);  // dwg_partial
+  accp(static_cast<size_t>(splits) * kDLCols * H * 4);  // dwg_partial (split-K partials)
+  accp((T + 127) / 128 * 128 * kDLCols * 2);  // dl_dense
+  accp(static_cast<size_t>(splits) * 4 * 2);  // rw_rows, rw_off
   accp(T * K * 4 * 5);    // topk_idx, intra_rank, topk_w, dl, slot_dst
   accp(nblk * E * 4 * 2);  // blk_hist, blk_base
   accp(E * N);            // layout
@@ -250,7 +254,10 @@ void allocate_rank(Layer& L, Rank& r) {
   r.dh = cp.take<__nv_bfloat16>(cap * 2 * F);
   r.wg = cp.take<__nv_bfloat16>(E * H);
   r.dwg = cp.take<float>(E * H);
-  r.dwg_partial = cp.take<float>(static_cast<size_t>(splits) * E * H);
+  r.dwg_partial = cp.take<float>(static_cast<size_t>(splits) * kDLCols * H);
+  r.dl_dense = cp.take<__nv_bfloat16>((T + 127) / 128 * 128 * kDLCols);
+  r.rw_rows = cp.take<int>(splits);
+  r.rw_off = cp.take<int>(splits);
   r.topk_idx = cp.take<int>(T * K);
   r.intra_rank = cp.take<int>(T * K);
   r.topk_w = cp.take<float>(T * K);
@@ -408,8 +415,10 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   const long long TH = static_cast<long long>(T) * H;
   for (size_t v = 0; v < L.ranks.size(); ++v) {
     Rank& r = L.ranks[v];
-    launch_combine_bwd(T, H, K, dy + (L.virt ? static_cast<long long>(v) * TH : 0), r.topk_w, r.slot_dst, L.peers,
-                       r.dl, st);
+    launch_combine_bwd(T, H, K, dy + (L.virt ? static_cast<long long>(v) * TH : 0), r.topk_w, r.topk_idx, r.slot_dst,
+                       L.peers, r.dl, r.dl_dense, r.rw_rows, r.rw_off, st);
+    launch_router_wgrad(r.x_in, T, H, E, r.dl_dense, L.T_max, r.rw_rows, r.rw_off, r.dwg_partial, r.dwg, L.num_sms,
+                        st);
   }
   mark(L, st, kPhCombineBwd);
   barrier(L, st);
@@ -453,7 +462,6 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
     Rank& r = L.ranks[v];
     launch_unpermute_bwd(T, H, K, r.topk_idx, r.dl, r.slot_dst, r.wg, L.peers,
                          dx + (L.virt ? static_cast<long long>(v) * TH : 0), st);
-    launch_router_wgrad(r.x_in, T, H, K, E, r.topk_idx, r.dl, r.dwg_partial, r.dwg, st);
   }
   mark(L, st, kPhUnpermute);
   if (N > 1)
