@@ -115,7 +115,8 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
   if (a.N % 32 != 0) throw std::runtime_error("grouped gemm: N must be a multiple of 32");
   if (!pair_gemm_supported(kind, a)) throw std::runtime_error("pair gemm: wgrad M must be a multiple of 256");
   GemmParams p{a.num_groups, a.group_rows, a.group_off, a.M,    a.N,    a.K,   a.out,
-               a.ldo,        a.out_group_stride, a.out2,    a.ldo2, a.aux, a.ld_aux, a.policy, a.raster};
+               a.ldo,        a.out_group_stride, a.out2,    a.ldo2, a.aux, a.ld_aux, a.policy, a.raster,
+               a.ready,      a.ready_epoch,      a.ready_n};
   switch (kind) {
     case GemmKind::kFwdGateUp: launch_pair<false, false, false, kEpiSwigluFwd>(tmA, tmB, p, num_sms, stream); break;
     case GemmKind::kFwdDown: launch_pair<false, false, false, kEpiBf16>(tmA, tmB, p, num_sms, stream); break;
@@ -130,7 +131,8 @@ void launch_grouped_gemm(GemmKind kind, const CUtensorMap& tmA, const CUtensorMa
   if (a.num_groups > gemm::MAX_GROUPS) throw std::runtime_error("grouped gemm: too many groups");
   if (a.N % 32 != 0) throw std::runtime_error("grouped gemm: N must be a multiple of 32");
   GemmParams p{a.num_groups, a.group_rows, a.group_off, a.M,    a.N,    a.K,   a.out,
-               a.ldo,        a.out_group_stride, a.out2,    a.ldo2, a.aux, a.ld_aux, a.policy, a.raster};
+               a.ldo,        a.out_group_stride, a.out2,    a.ldo2, a.aux, a.ld_aux, a.policy, a.raster,
+               a.ready,      a.ready_epoch,      a.ready_n};
   switch (kind) {
     case GemmKind::kFwdGateUp: launch_one<false, false, false, kEpiSwigluFwd>(tmA, tmB, p, num_sms, stream); break;
     case GemmKind::kFwdDown: launch_one<false, false, false, kEpiBf16>(tmA, tmB, p, num_sms, stream); break;

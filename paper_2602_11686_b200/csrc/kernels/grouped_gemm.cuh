@@ -48,7 +48,28 @@ struct GemmParams {
   long long ld_aux;
   int policy;  // L2 hints: bits 0-1 A, bits 2-3 B (0 default for the mode, 1 normal, 2 evict_first, 3 evict_last)
   int raster;  // tile order within a group: 0 mode default, 1 m-inner, 2 n-inner, 3+ = m-chunks of `raster` tiles, n-inner
+  // Optional per-group readiness (M-grouped only): before loading B of group g the
+  // producer waits until ready[g * ready_n + q] has reached ready_epoch for all
+  // q < ready_n (restored expert chunks landing from the copy engines).
+  const unsigned* ready;
+  unsigned ready_epoch;
+  int ready_n;
 };
+
+__device__ __forceinline__ void wait_group_ready(const GemmParams& p, int g) {
+  if (p.ready == nullptr) return;
+  for (int q = 0; q < p.ready_n; ++q) {
+    const unsigned* f = p.ready + g * p.ready_n + q;
+    while (true) {
+      unsigned v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if (static_cast<int>(v - p.ready_epoch) >= 0) break;
+      __nanosleep(256);
+    }
+  }
+  // the chunks were written by copy engines (generic proxy); TMA reads via the async proxy
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 
 namespace gemm {
 constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
@@ -168,11 +189,16 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
       const uint64_t pol_b = kGroupK ? policy_evict_last() : policy_evict_first();
       int s = 0;
       uint32_t ph = 0;
+      int ready_g = -1;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         int g, mb, nbk;
         decode(t, g, mb, nbk);
         const int nk = k_blocks(g);
         const int row0 = p.group_off[g];
+        if (!kGroupK && g != ready_g) {
+          wait_group_ready(p, g);
+          ready_g = g;
+        }
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* sA = smem + s * STAGE_BYTES;

@@ -106,11 +106,16 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
       const uint64_t pol_b = pick_policy(((p.policy >> 2) & 3) ? ((p.policy >> 2) & 3) : 3, false);
       int s = 0;
       uint32_t ph = 0;
+      int ready_g = -1;
       for (int t = cluster; t < total_tiles; t += nclusters) {
         int g, mb, nbk;
         decode(t, g, mb, nbk);
         const int nk = k_blocks(g);
         const int row0 = p.group_off[g];
+        if (!kGroupK && g != ready_g) {
+          wait_group_ready(p, g);
+          ready_g = g;
+        }
         const int m_half = mb * BM + rank * HALF;   // this CTA's first A row (M-grouped: within the group)
         const int n_half = nbk * BN + rank * HALF;  // this CTA's first B column
         for (int kb = 0; kb < nk; ++kb) {

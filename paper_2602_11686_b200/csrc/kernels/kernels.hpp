@@ -31,6 +31,9 @@ struct GroupedGemmArgs {
   long long ld_aux;
   int policy = 0;  // see GemmParams
   int raster = 0;
+  const unsigned* ready = nullptr;  // per-group readiness flags (see GemmParams)
+  unsigned ready_epoch = 0;
+  int ready_n = 0;
 };
 
 enum class GemmKind : int {

@@ -392,6 +392,36 @@ __global__ void grad_reduce_scatter_kernel(const PlanTables* __restrict__ pt, Pe
   }
 }
 
+// Owner-side sum of the grad reduce-scatter when the replicas' chunks were
+// gathered by copy engines into stage[e][h] (h = hosting device): ascending-device
+// order, the local replica read in place.  Deterministic, HBM-bound.
+__global__ void grad_rs_sum_kernel(const PlanTables* __restrict__ pt, const float* __restrict__ grad_full,
+                                   const float* __restrict__ stage, int N, int rank, long long S, long long flat,
+                                   float* __restrict__ grad_shard) {
+  const int e = blockIdx.y;
+  const int nh = pt->n_hosts[e];
+  const float4* src[kMaxRanks];
+  for (int h = 0; h < nh; ++h) {
+    const int d = pt->host_dev[e][h];
+    src[h] = d == rank ? reinterpret_cast<const float4*>(grad_full + static_cast<long long>(pt->slot_of[e][d]) * flat +
+                                                         static_cast<long long>(rank) * S)
+                       : reinterpret_cast<const float4*>(stage + (static_cast<long long>(e) * N + d) * S);
+  }
+  float4* dst = reinterpret_cast<float4*>(grad_shard + static_cast<long long>(e) * S);
+  const long long n = S / 4;
+  for (long long i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float4 a = src[0][i];
+    for (int h = 1; h < nh; ++h) {
+      const float4 b = src[h][i];
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+    }
+    dst[i] = a;
+  }
+}
+
 // ------------------------------------------------------------ weight packing
 // flat[3HF] = [W13 interleaved: rows 256b+q (q<128) = w1[128b+q], 256b+128+q = w3[128b+q]; W2]
 __global__ void pack_expert_kernel(const __nv_bfloat16* __restrict__ w1, const __nv_bfloat16* __restrict__ w3,
@@ -541,4 +571,12 @@ void launch_unpack_grad(const float* chunk, long long lo, long long hi, int H, i
   count_launch();
 }
 
+}  // namespace fsep
+
+namespace fsep {
+void launch_grad_rs_sum(const PlanTables* pt, const float* grad_full, const float* stage, int E, int N, int rank,
+                        long long S, long long flat, float* grad_shard, cudaStream_t st) {
+  grad_rs_sum_kernel<<<dim3(128, E), 256, 0, st>>>(pt, grad_full, stage, N, rank, S, flat, grad_shard);
+  count_launch();
+}
 }  // namespace fsep

@@ -52,6 +52,8 @@ void launch_router_wgrad(const __nv_bfloat16* x, int T, int H, int E, const __nv
                          cudaStream_t st);
 void launch_grad_reduce_scatter(const PlanTables* pt, const PeerTable& peers, int E, int rank, long long S,
                                 long long flat, float* grad_shard, cudaStream_t st);
+void launch_grad_rs_sum(const PlanTables* pt, const float* grad_full, const float* stage, int E, int N, int rank,
+                        long long S, long long flat, float* grad_shard, cudaStream_t st);
 void launch_pack_expert(const __nv_bfloat16* w1, const __nv_bfloat16* w3, const __nv_bfloat16* w2, int H, int F,
                         __nv_bfloat16* flat, cudaStream_t st);
 void launch_unpack_grad(const float* chunk, long long lo, long long hi, int H, int F, float* dw1, float* dw3,

@@ -130,6 +130,18 @@ extern "C" struct mp_fsep_layer {
   uint64_t launches_before = 0, launches_step = 0;
   double gemm_flops_step = 0.0;
   int restore_blocks = 32;  // CTAs per (slot, peer) chunk of the restore kernel
+  // Copy-engine communication (real mode, N > 1): shard restore and the grad
+  // reduce-scatter gathers run as peer cudaMemcpyAsync on one stream per peer,
+  // using no SMs; the forward GEMMs poll per-(slot, peer) readiness flags.
+  bool ce_mode = false;
+  cudaStream_t ce[kMaxRanks] = {};
+  cudaEvent_t ev_ce[kMaxRanks] = {};
+  cudaEvent_t ev_wg = nullptr;
+  unsigned* d_ready = nullptr;  // [kMaxExperts][kMaxRanks]
+  unsigned restore_epoch = 0;
+  uint8_t* layout_ring = nullptr;  // pinned [4][E*N] host snapshots of the layout per forward
+  const uint8_t* cur_layout = nullptr;
+  float* rs_stage = nullptr;  // [E][N][S] gathered replica chunks (owner side)
   // optional per-phase event timing (FSEP_PHASE_TIMING=1)
   static constexpr int kPhaseRing = 64;
   bool phase_on = false;
@@ -158,6 +170,28 @@ enum Phase : int {
   kPhRestoreEnd,
   kPhCount
 };
+
+// cuStreamWriteValue32 through the runtime's driver entry point (no libcuda link).
+using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteValueFn write_value_fn() {
+  static WriteValueFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<WriteValueFn>(nullptr);
+    return reinterpret_cast<WriteValueFn>(p);
+  }();
+  return fn;
+}
+
+// Ascending list of experts hosted by device d under layout A (E x N).
+std::vector<int> hosted_experts(const uint8_t* A, int E, int N, int d) {
+  std::vector<int> out;
+  for (int e = 0; e < E; ++e)
+    if (A[e * N + d]) out.push_back(e);
+  return out;
+}
 
 void mark(mp_fsep_layer& L, cudaStream_t st, int phase) {
   if (!L.phase_on) return;
@@ -323,15 +357,48 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   L.T_step = T;
   const long long TH = static_cast<long long>(T) * H;
   // 1. layout for this step (planner result of the previous step, or set_layout)
-  if (L.planner_pending) CK(cudaStreamWaitEvent(st, L.ev_planned, 0));
-  for (Rank& r : L.ranks) CK(cudaMemcpyAsync(r.layout_dev, L.layout_host, static_cast<size_t>(E) * N, cudaMemcpyHostToDevice, st));
-  // 2. shard restore on the side stream (overlaps router + dispatch)
+  const bool ce = L.ce_mode;
+  if (ce) {
+    // Copy-engine restore needs the layout on the host: wait for the previous
+    // step's planner callback (it ran right after that step's router, so the
+    // host stays up to one step ahead) and snapshot it for this step.
+    if (L.planner_pending) CK(cudaEventSynchronize(L.ev_planned));
+    uint8_t* snap = L.layout_ring + (L.step_no % 4) * static_cast<size_t>(E) * N;
+    std::memcpy(snap, L.layout_host, static_cast<size_t>(E) * N);
+    L.cur_layout = snap;
+    for (Rank& r : L.ranks) CK(cudaMemcpyAsync(r.layout_dev, snap, static_cast<size_t>(E) * N, cudaMemcpyHostToDevice, st));
+  } else {
+    if (L.planner_pending) CK(cudaStreamWaitEvent(st, L.ev_planned, 0));
+    for (Rank& r : L.ranks)
+      CK(cudaMemcpyAsync(r.layout_dev, L.layout_host, static_cast<size_t>(E) * N, cudaMemcpyHostToDevice, st));
+  }
+  // 2. shard restore on the side stream(s) (overlaps router + dispatch, and in
+  //    copy-engine mode the forward GEMMs too: they wait per slot, not per step)
   const bool restore = N > 1 && L.restore_every_step;
   mark(L, st, kPhFwdBegin);
   // peers' shards must be final (parameter load / optimizer update) before anyone gathers them
   barrier(L, st);
   mark(L, st, kPhParamBarrier);
-  if (restore) {
+  if (restore && ce) {
+    Rank& r = L.ranks[0];
+    const std::vector<int> mine = hosted_experts(L.cur_layout, E, N, r.rank);
+    ++L.restore_epoch;
+    CK(cudaEventRecord(L.ev_fork, st));
+    mark(L, st, kPhRestoreBegin);
+    for (int q = 0; q < N; ++q) {
+      const int p = (r.rank + q) % N;  // start with the local chunk, then peers in ring order
+      CK(cudaStreamWaitEvent(L.ce[p], L.ev_fork, 0));
+      for (int c = 0; c < static_cast<int>(mine.size()); ++c) {
+        CK(cudaMemcpyAsync(r.restored + static_cast<long long>(c) * L.flat + static_cast<long long>(p) * L.S,
+                           L.peers.shard[p] + static_cast<long long>(mine[c]) * L.S, static_cast<size_t>(L.S) * 2,
+                           cudaMemcpyDeviceToDevice, L.ce[p]));
+        if (write_value_fn()(L.ce[p], reinterpret_cast<CUdeviceptr>(L.d_ready + c * N + p), L.restore_epoch, 0) !=
+            CUDA_SUCCESS)
+          throw Error(ErrorKind::device, "cuStreamWriteValue32 failed");
+      }
+      CK(cudaEventRecord(L.ev_ce[p], L.ce[p]));
+    }
+  } else if (restore) {
     CK(cudaEventRecord(L.ev_fork, st));
     CK(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
     mark(L, L.side, kPhRestoreBegin);
@@ -379,11 +446,16 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   barrier(L, st);
   mark(L, st, kPhDispatchBarrier);
   // 5. expert FFN on the restored experts
-  if (restore) CK(cudaStreamWaitEvent(st, L.ev_restored, 0));
+  if (restore && !ce) CK(cudaStreamWaitEvent(st, L.ev_restored, 0));
   mark(L, st, kPhRestoreWait);
   CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][0], st));
   for (Rank& r : L.ranks) {
     GroupedGemmArgs g = gemm_args(L, r);
+    if (restore && ce) {  // per-(slot, peer) readiness instead of a whole-restore join
+      g.ready = L.d_ready;
+      g.ready_epoch = L.restore_epoch;
+      g.ready_n = N;
+    }
     g.N = 2 * F;
     g.K = H;
     g.out = r.h;
@@ -391,12 +463,18 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
     g.out2 = r.act;
     g.ldo2 = F;
     gemm(L, GemmKind::kFwdGateUp, r.tm_x_k, r.tm_w13_k, r.tm_w13_k128, g, st);
-    GroupedGemmArgs g2 = gemm_args(L, r);
+    GroupedGemmArgs g2 = g;
     g2.N = H;
     g2.K = F;
     g2.out = r.y_rows;
     g2.ldo = H;
+    g2.out2 = nullptr;
+    g2.ldo2 = 0;
     gemm(L, GemmKind::kFwdDown, r.tm_act_k, r.tm_w2_k, r.tm_w2_k128, g2, st);
+  }
+  if (restore && ce) {
+    for (int p = 0; p < N; ++p) CK(cudaStreamWaitEvent(st, L.ev_ce[p], 0));  // join (long complete)
+    mark(L, st, kPhRestoreEnd);
   }
   CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][1], st));
   mark(L, st, kPhFwdGemm);
@@ -424,6 +502,8 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   barrier(L, st);
   mark(L, st, kPhCombineBwdBarrier);
   CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][2], st));
+  // Weight gradients first: in copy-engine mode their reduce-scatter gathers run
+  // on the copy engines underneath the (long) dX GEMM that follows.
   for (Rank& r : L.ranks) {
     GroupedGemmArgs g = gemm_args(L, r);  // dAct -> dH (SwiGLU backward fused)
     g.N = F;
@@ -433,12 +513,6 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
     g.aux = r.h;
     g.ld_aux = 2 * F;
     gemm(L, GemmKind::kBwdDownDgrad, r.tm_dy_k, r.tm_w2_mn, r.tm_w2_mn, g, st);
-    GroupedGemmArgs g2 = gemm_args(L, r);  // dX rows
-    g2.N = H;
-    g2.K = 2 * F;
-    g2.out = r.dx_rows;
-    g2.ldo = H;
-    gemm(L, GemmKind::kBwdUpDgrad, r.tm_dh_k, r.tm_w13_mn, r.tm_w13_mn, g2, st);
     GroupedGemmArgs g3 = gemm_args(L, r);  // dW2 = dY^T act
     g3.M = H;
     g3.N = F;
@@ -454,8 +528,37 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
     g4.out_group_stride = L.flat;
     gemm(L, GemmKind::kBwdWgrad, r.tm_dh_mn, r.tm_x_mn, r.tm_x_mn, g4, st);
   }
+  const bool ce_rs = L.ce_mode && N > 1;
+  if (ce_rs) {
+    barrier(L, st);  // every rank's replica gradients are complete
+    CK(cudaEventRecord(L.ev_wg, st));
+    Rank& r = L.ranks[0];
+    for (int q = 1; q < N; ++q) {
+      const int h = (r.rank + q) % N;
+      const std::vector<int> theirs = hosted_experts(L.cur_layout, E, N, h);
+      CK(cudaStreamWaitEvent(L.ce[h], L.ev_wg, 0));
+      for (int c = 0; c < static_cast<int>(theirs.size()); ++c)
+        CK(cudaMemcpyAsync(L.rs_stage + (static_cast<long long>(theirs[c]) * N + h) * L.S,
+                           L.peers.grad_full[h] + static_cast<long long>(c) * L.flat + static_cast<long long>(r.rank) * L.S,
+                           static_cast<size_t>(L.S) * 4, cudaMemcpyDeviceToDevice, L.ce[h]));
+      CK(cudaEventRecord(L.ev_ce[h], L.ce[h]));
+    }
+  }
+  for (Rank& r : L.ranks) {
+    GroupedGemmArgs g2 = gemm_args(L, r);  // dX rows
+    g2.N = H;
+    g2.K = 2 * F;
+    g2.out = r.dx_rows;
+    g2.ldo = H;
+    gemm(L, GemmKind::kBwdUpDgrad, r.tm_dh_k, r.tm_w13_mn, r.tm_w13_mn, g2, st);
+  }
   CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][3], st));
   mark(L, st, kPhBwdGemm);
+  if (ce_rs) {
+    Rank& r = L.ranks[0];
+    for (int q = 1; q < N; ++q) CK(cudaStreamWaitEvent(st, L.ev_ce[(r.rank + q) % N], 0));
+    launch_grad_rs_sum(r.pt, r.grad_full, L.rs_stage, E, N, r.rank, L.S, L.flat, r.grad_shard, st);
+  }
   barrier(L, st);
   mark(L, st, kPhBwdGemmBarrier);
   for (size_t v = 0; v < L.ranks.size(); ++v) {
@@ -464,7 +567,7 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
                          dx + (L.virt ? static_cast<long long>(v) * TH : 0), st);
   }
   mark(L, st, kPhUnpermute);
-  if (N > 1)
+  if (N > 1 && !ce_rs)
     for (Rank& r : L.ranks) launch_grad_reduce_scatter(r.pt, L.peers, E, r.rank, L.S, L.flat, r.grad_shard, st);
   mark(L, st, kPhGradRS);
   // join the planner stream (it finished long before the backward GEMMs did)
@@ -553,6 +656,20 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
         for (auto& e : ring) CK(cudaEventCreate(&e));
     }
     if (const char* v = std::getenv("FSEP_RESTORE_BLOCKS")) L->restore_blocks = std::max(1, std::atoi(v));
+    // copy-engine communication for real multi-GPU mode (FSEP_COMM=kernel selects the SM kernels)
+    const char* comm = std::getenv("FSEP_COMM");
+    L->ce_mode = !L->virt && L->N > 1 && !(comm && std::string(comm) == "kernel") && write_value_fn() != nullptr;
+    if (L->ce_mode) {
+      for (int p = 0; p < L->N; ++p) {
+        CK(cudaStreamCreateWithFlags(&L->ce[p], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&L->ev_ce[p], cudaEventDisableTiming));
+      }
+      CK(cudaEventCreateWithFlags(&L->ev_wg, cudaEventDisableTiming));
+      CK(cudaMalloc(&L->d_ready, sizeof(unsigned) * kMaxExperts * kMaxRanks));
+      CK(cudaMemset(L->d_ready, 0, sizeof(unsigned) * kMaxExperts * kMaxRanks));
+      CK(cudaMallocHost(&L->layout_ring, 4 * static_cast<size_t>(L->E) * L->N));
+      CK(cudaMalloc(&L->rs_stage, static_cast<size_t>(L->E) * L->N * static_cast<size_t>(L->S) * sizeof(float)));
+    }
     CK(cudaMalloc(&L->d_peer_flags, sizeof(unsigned int*) * kMaxRanks));
     if (L->virt) {
       unsigned int* f[kMaxRanks] = {};
@@ -580,6 +697,16 @@ void mp_fsep_layer_free(mp_fsep_layer* L) {
   cudaStreamDestroy(L->side);
   cudaStreamDestroy(L->plan_stream);
   cudaStreamDestroy(L->cap_stream);
+  if (L->ce_mode) {
+    for (int p = 0; p < L->N; ++p) {
+      cudaStreamDestroy(L->ce[p]);
+      cudaEventDestroy(L->ev_ce[p]);
+    }
+    cudaEventDestroy(L->ev_wg);
+    cudaFree(L->d_ready);
+    cudaFreeHost(L->layout_ring);
+    cudaFree(L->rs_stage);
+  }
   for (cudaEvent_t e : {L->ev_fork, L->ev_restored, L->ev_hist, L->ev_planned}) cudaEventDestroy(e);
   for (auto& ring : L->ev_g)
     for (auto e : ring) cudaEventDestroy(e);
@@ -886,6 +1013,15 @@ mp_status mp_fsep_layer_graph_step(mp_fsep_layer* L, const void* x, const float*
       // on inside a capture: settle the planner first.
       if (L->planner_pending) CK(cudaEventSynchronize(L->ev_planned));
       L->planner_pending = false;
+      // A captured graph must not bake layout-dependent copy addresses: graphs use
+      // the device-side (layout read on the GPU) restore / reduce-scatter kernels.
+      const bool ce_saved = L->ce_mode;
+      L->ce_mode = false;
+      struct Restore {
+        mp_fsep_layer* l;
+        bool v;
+        ~Restore() { l->ce_mode = v; }
+      } restore_ce{L, ce_saved};
       cudaStream_t cs = L->cap_stream;
       CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
       const uint64_t l0 = launches_issued();
