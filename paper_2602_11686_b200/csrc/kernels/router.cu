@@ -207,23 +207,39 @@ __global__ void __launch_bounds__(kBlockTokens) router_small_kernel(
   constexpr int kWords = BT / 32;
   __shared__ int s_idx[BT][8];
   __shared__ unsigned s_mask[E_][kWords];
+  extern __shared__ uint4 s_w4[];  // the whole router weight [E_][H] bf16 (64 KB for E=8, H=4096)
   const int tt = threadIdx.x;
   const int t = blockIdx.x * BT + tt;
+  const int pieces = H / 8;
   for (int i = tt; i < E_ * kWords; i += BT) (&s_mask[0][0])[i] = 0u;
+  for (int i = tt; i < E_ * pieces; i += BT) s_w4[i] = __ldg(reinterpret_cast<const uint4*>(wg) + i);
   __syncthreads();
   if (t < T) {
     float acc[E_];
 #pragma unroll
     for (int e = 0; e < E_; ++e) acc[e] = 0.f;
     const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * H);
-    const uint4* wr = reinterpret_cast<const uint4*>(wg);
-    const int pieces = H / 8;
-#pragma unroll 2
-    for (int p = 0; p < pieces; ++p) {
+    // 8-deep register prefetch ring over the token row: each thread streams its
+    // own row, so memory-level parallelism has to come from the ring, not from
+    // the (few) resident warps.
+    constexpr int D = 8;
+    uint4 ring[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) ring[i] = __ldg(xr + i);
+    for (int p0 = 0; p0 < pieces; p0 += D) {
+      uint4 cur[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) cur[i] = ring[i];
+      if (p0 + D < pieces) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) ring[i] = __ldg(xr + p0 + D + i);
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+      const int p = p0 + i;
       float xf[8];
       {
-        const uint4 q = __ldg(xr + p);
-        const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+        const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&cur[i]);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const float2 f = __bfloat1622float2(b[k]);
@@ -233,7 +249,7 @@ __global__ void __launch_bounds__(kBlockTokens) router_small_kernel(
       }
 #pragma unroll
       for (int e = 0; e < E_; ++e) {
-        const uint4 q = __ldg(wr + static_cast<size_t>(e) * pieces + p);
+        const uint4 q = s_w4[e * pieces + p];
         const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -241,6 +257,7 @@ __global__ void __launch_bounds__(kBlockTokens) router_small_kernel(
           acc[e] = __fmaf_rn(xf[2 * k], f.x, acc[e]);
           acc[e] = __fmaf_rn(xf[2 * k + 1], f.y, acc[e]);
         }
+      }
       }
     }
     if (bias) {
@@ -314,12 +331,19 @@ void launch_router(const RouterArgs& a, cudaStream_t st) {
   if (nblk == 0) return;
   if (a.E % 8 != 0 || a.E > kMaxExperts) throw std::runtime_error("router: n_experts must be a multiple of 8, <= 128");
   if (a.H % kHC != 0) throw std::runtime_error("router: hidden must be a multiple of 64");
-  if (a.E == 8)
-    router_small_kernel<8><<<nblk, kBlockTokens, 0, st>>>(a.x, a.wg, a.bias, a.T, a.H, a.K, a.topk_idx, a.topk_w,
-                                                         a.intra_rank, a.blk_hist);
-  else if (a.E == 16)
-    router_small_kernel<16><<<nblk, kBlockTokens, 0, st>>>(a.x, a.wg, a.bias, a.T, a.H, a.K, a.topk_idx, a.topk_w,
-                                                          a.intra_rank, a.blk_hist);
+  const size_t w_bytes = static_cast<size_t>(a.E) * a.H * sizeof(__nv_bfloat16);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(router_small_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(router_small_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  if (a.E == 8 && w_bytes <= 200 * 1024)
+    router_small_kernel<8><<<nblk, kBlockTokens, w_bytes, st>>>(a.x, a.wg, a.bias, a.T, a.H, a.K, a.topk_idx,
+                                                               a.topk_w, a.intra_rank, a.blk_hist);
+  else if (a.E == 16 && w_bytes <= 200 * 1024)
+    router_small_kernel<16><<<nblk, kBlockTokens, w_bytes, st>>>(a.x, a.wg, a.bias, a.T, a.H, a.K, a.topk_idx,
+                                                                a.topk_w, a.intra_rank, a.blk_hist);
   else
     launch_tiled<4, 4>(a, nblk, st);  // 16 x E/4 threads, register-tiled
   count_launch();
