@@ -76,6 +76,14 @@ mp_status mp_fsep_time_cost(uint32_t n_devices, uint32_t n_experts, const uint64
  * Drives the routing bias of the multi-layer dynamic-skew benchmark. */
 mp_status mp_fsep_trace_popularity(const char* spec_json, double* out, uint64_t capacity);
 
+/* Trace export: build an mp_trace from observed histograms (e.g. every step's
+ * mp_fsep_layer_histogram) and write it with mp_trace_save in the reference
+ * JSONL format {"iter","layer","R"} (trace.cpp:220-235), so the reference
+ * tooling (mp_simulate / mp_plan_layer_json / moeplan simulate) replays real
+ * B200 routing.  Records must be unique per (iter, layer). */
+mp_status mp_fsep_trace_create(uint32_t n_devices, uint32_t n_experts, mp_trace** out);
+mp_status mp_fsep_trace_append(mp_trace* trace, uint32_t iteration, uint32_t layer, const uint64_t* R);
+
 /* ========================= GPU FSEP layer step ============================= */
 
 typedef struct mp_fsep_layer mp_fsep_layer;
@@ -161,11 +169,11 @@ mp_status mp_fsep_layer_read(mp_fsep_layer* layer, const char* name, uint32_t vr
 mp_status mp_fsep_layer_stats(mp_fsep_layer* layer, uint64_t* kernel_launches, double* gemm_ms, double* gemm_flops);
 mp_status mp_fsep_layer_stats_reset(mp_fsep_layer* layer);
 /* Per-phase mean times (ms) since the last reset, when the layer was created with
- * FSEP_PHASE_TIMING=1 in the environment.  out[0..14]: consecutive main-stream
- * phases (param barrier, router+scan, R barrier, plan+dispatch, dispatch barrier,
- * restore wait, fwd GEMMs, barrier, combine, combine-bwd, barrier, bwd GEMMs,
- * barrier, unpermute+router wgrad, grad reduce-scatter); out[15] whole step;
- * out[16] restore start offset; out[17] restore duration (side stream).  n >= 18. */
+ * FSEP_PHASE_TIMING=1 in the environment.  out[0..15]: consecutive main-stream
+ * phases (param barrier, router+scan, R barrier, plan, dispatch, dispatch barrier,
+ * restore wait, fwd GEMMs, barrier, combine, combine-bwd + router wgrad, barrier,
+ * bwd GEMMs, barrier, unpermute, grad reduce-scatter); out[16] whole step;
+ * out[17] restore start offset; out[18] restore duration.  n >= 19. */
 mp_status mp_fsep_layer_phase_ms(mp_fsep_layer* layer, double* out, uint32_t n);
 
 /* Capture forward+backward into a CUDA graph and replay it (bench path). */

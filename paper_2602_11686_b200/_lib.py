@@ -74,6 +74,8 @@ _SIGS = {
     "mp_fsep_time_cost": (C.c_int, [u32, u32, u64p, u8p, C.c_double, C.c_double, C.c_double, C.c_double,
                                     dblp, dblp, dblp, u64p]),
     "mp_fsep_trace_popularity": (C.c_int, [cp, dblp, u64]),
+    "mp_fsep_trace_create": (C.c_int, [u32, u32, C.POINTER(vp)]),
+    "mp_fsep_trace_append": (C.c_int, [vp, u32, u32, u64p]),
     # moeplan_fsep.h -- GPU layer
     "mp_fsep_layer_create": (C.c_int, [C.POINTER(FsepDesc), C.c_int, C.POINTER(vp)]),
     "mp_fsep_layer_free": (None, [vp]),

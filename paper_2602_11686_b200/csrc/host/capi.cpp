@@ -1,6 +1,7 @@
 // C ABI of the host planner: the reference's mp_* surface
 // (/root/reference/proj/include/moeplan.h:46-107) plus the array-level
 // mp_fsep_* planner entry points declared in include/moeplan_fsep.h.
+#include <algorithm>
 #include <limits>
 #include <memory>
 #include <vector>
@@ -20,6 +21,7 @@ extern "C" {
 struct mp_trace {
   std::vector<TraceRecord> records;
   std::vector<std::uint32_t> layers;
+  std::uint32_t n_devices = 0, n_experts = 0;  // for traces built by mp_fsep_trace_append
 };
 struct mp_config {
   RunConfig cfg;
@@ -280,6 +282,39 @@ mp_status mp_fsep_even_layout(uint32_t n_devices, uint32_t n_experts, uint32_t c
     require(A_out, "mp_fsep_even_layout: NULL argument");
     const Topology topo(1, static_cast<int>(n_devices), 1.0, 1.0);
     layout_to(even_replication_layout(topo, static_cast<int>(n_experts), static_cast<int>(capacity)), A_out);
+  });
+}
+
+mp_status mp_fsep_trace_create(uint32_t n_devices, uint32_t n_experts, mp_trace** out) {
+  return guarded([&] {
+    require(out && n_devices > 0 && n_experts > 0, "mp_fsep_trace_create: bad argument");
+    auto* t = make_trace({});
+    t->n_devices = n_devices;
+    t->n_experts = n_experts;
+    *out = t;
+  });
+}
+
+mp_status mp_fsep_trace_append(mp_trace* trace, uint32_t iteration, uint32_t layer, const uint64_t* R) {
+  return guarded([&] {
+    require(trace && R, "mp_fsep_trace_append: NULL argument");
+    uint32_t n = trace->n_devices, e = trace->n_experts;
+    if (!trace->records.empty()) {
+      n = static_cast<uint32_t>(trace->records.front().routing.n_devices());
+      e = static_cast<uint32_t>(trace->records.front().routing.n_experts());
+    }
+    require(n > 0 && e > 0, "mp_fsep_trace_append: trace has no dimensions (use mp_fsep_trace_create)");
+    for (const TraceRecord& r : trace->records)
+      require(!(r.iteration == iteration && r.layer == layer), "mp_fsep_trace_append: duplicate (iter, layer) pair");
+    TraceRecord rec;
+    rec.iteration = iteration;
+    rec.layer = layer;
+    rec.routing = matrix_from(R, n, e);
+    trace->records.push_back(std::move(rec));
+    std::sort(trace->records.begin(), trace->records.end(), [](const TraceRecord& a, const TraceRecord& b) {
+      return a.iteration != b.iteration ? a.iteration < b.iteration : a.layer < b.layer;
+    });
+    trace->layers = distinct_layers(trace->records);
   });
 }
 

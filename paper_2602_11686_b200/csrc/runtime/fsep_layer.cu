@@ -2,20 +2,25 @@
 // mp_fsep_layer_* C ABI (include/moeplan_fsep.h).
 //
 // Step schedule (per rank; in virtual mode every phase loops over the N
-// emulated ranks on one GPU, in real mode a peer barrier separates phases):
-//   forward   layout H2D (from the planner) | restore (side stream, peer reads)
+// emulated ranks on one GPU, in real mode a peer barrier kernel separates phases):
+//   forward   layout H2D | == barrier == | shard restore (copy engines, one stream
+//             per peer, per-(slot, peer) readiness flags; virtual mode: a restore
+//             kernel on a side stream)
 //             router+top-k+histogram -> block scan (R row -> every rank's R_all)
 //             == barrier ==  plan (device lite routing) + pad zeroing
-//             dispatch (token rows -> destination rows, peer stores)
-//             == barrier ==  [wait restore] GEMM gate/up + SwiGLU -> GEMM down
-//             == barrier ==  combine (peer loads, gate-weighted fp32 sum)
 //             R D2H + host planner callback (planner stream) -> layout of step t+1
-//   backward  combine bwd (dw, dl; dY rows -> expert devices)
-//             == barrier ==  dgrad (SwiGLU') x2, wgrad x2 (fp32)
-//             == barrier ==  unpermute bwd (+ router dx), router wgrad,
-//             grad reduce-scatter into the fp32 shards (peer loads)
-// Nothing in the step needs a host synchronisation: the layout travels
-// host->device as a stream-ordered copy, the per-expert row counts never leave
+//             dispatch (token rows -> destination rows, peer stores)
+//             == barrier ==  GEMM gate/up + SwiGLU -> GEMM down (producer waits per
+//             slot for its restored chunks, so the restore overlaps the GEMMs)
+//             == barrier ==  combine (peer loads, gate-weighted fp32 sum)
+//   backward  combine bwd (dw, dl; dY rows -> expert devices) + router wgrad GEMM
+//             == barrier ==  dgrad (SwiGLU'), wgrad x2 (fp32)
+//             == barrier ==  grad reduce-scatter gathers on the copy engines, under
+//             the dX GEMM that follows; owner-side sum kernel
+//             == barrier ==  unpermute bwd (+ router dx)
+// Only the copy-engine path needs the layout on the host: the forward waits on
+// the previous step's planner callback (which ran right after that step's
+// router), so the host stays one step ahead.  Per-expert row counts never leave
 // the device (the grouped GEMMs schedule their tiles from them).
 #include <cuda_runtime.h>
 #include <nccl.h>
@@ -145,7 +150,7 @@ extern "C" struct mp_fsep_layer {
   // optional per-phase event timing (FSEP_PHASE_TIMING=1)
   static constexpr int kPhaseRing = 64;
   bool phase_on = false;
-  std::vector<std::array<cudaEvent_t, 20>> ev_p;
+  std::vector<std::array<cudaEvent_t, 24>> ev_p;
 };
 
 namespace {
@@ -154,6 +159,7 @@ enum Phase : int {
   kPhParamBarrier,
   kPhRouter,
   kPhRBarrier,
+  kPhPlan,
   kPhDispatch,
   kPhDispatchBarrier,
   kPhRestoreWait,
@@ -424,6 +430,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
     launch_plan(r.R_all, r.layout_dev, E, N, r.rank, r.pt, L.cap, st);
     launch_zero_pad(r.pt, C, H, r.x_rows, r.dy_rows, st);
   }
+  mark(L, st, kPhPlan);
   // histogram -> host planner (async, off the critical path)
   CK(cudaMemcpyAsync(L.R_host, L.ranks[0].R_all, static_cast<size_t>(N) * E * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaEventRecord(L.ev_hist, st));

@@ -156,14 +156,15 @@ class FsepLayer:
         check(self.lib.mp_fsep_layer_stats(self._h, C.byref(n), C.byref(ms), C.byref(fl)))
         return {"kernel_launches": n.value, "gemm_ms": ms.value, "gemm_flops": fl.value}
 
-    PHASES = ["param_barrier", "router_scan", "R_barrier", "plan_dispatch", "dispatch_barrier", "restore_wait",
-              "fwd_gemms", "fwd_barrier", "combine", "combine_bwd", "bwd_barrier0", "bwd_gemms", "bwd_barrier1",
-              "unpermute_router_wgrad", "grad_reduce_scatter", "step_total", "restore_start", "restore_ms"]
+    PHASES = ["param_barrier", "router_scan", "R_barrier", "plan", "dispatch", "dispatch_barrier", "restore_wait",
+              "fwd_gemms", "fwd_barrier", "combine", "combine_bwd_router_wgrad", "bwd_barrier0", "bwd_gemms",
+              "rs_sum_barrier", "unpermute", "grad_reduce_scatter_kernel", "step_total", "restore_start",
+              "restore_ms"]
 
     def phase_ms(self):
         """Mean per-phase device times (needs FSEP_PHASE_TIMING=1 at layer creation), or None."""
-        out = (C.c_double * 18)()
-        if self.lib.mp_fsep_layer_phase_ms(self._h, out, 18) != 0:
+        out = (C.c_double * 19)()
+        if self.lib.mp_fsep_layer_phase_ms(self._h, out, 19) != 0:
             return None
         return {k: round(out[i], 4) for i, k in enumerate(self.PHASES)}
 

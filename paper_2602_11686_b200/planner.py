@@ -81,6 +81,17 @@ class Trace:
         check(load().mp_trace_load(str(path).encode(), C.byref(h)))
         return cls(h)
 
+    @classmethod
+    def create(cls, n_devices: int, n_experts: int) -> "Trace":
+        """Empty trace to record observed histograms (mp_fsep_trace_create)."""
+        h = C.c_void_p()
+        check(load().mp_fsep_trace_create(n_devices, n_experts, C.byref(h)))
+        return cls(h)
+
+    def append(self, iteration: int, layer: int, R) -> None:
+        R = _u64(R)
+        check(load().mp_fsep_trace_append(self._h, iteration, layer, _p64(R)))
+
     def save(self, path: str) -> None:
         check(load().mp_trace_save(self._h, str(path).encode()))
 

@@ -137,3 +137,26 @@ def test_trace_popularity_rounds_to_generated_trace(product_lib):
         exact = pop[rec["layer"], rec["iter"]] * 10000
         load = np.array(rec["expert_load"]) / 2
         assert (np.abs(load - exact) < 1.0 + 1e-9).all()
+
+
+def test_trace_export_replays_on_reference(product_lib, ref, tmp_path):
+    """Histograms recorded through mp_fsep_trace_append save in the reference JSONL
+    format; the reference library replays them to byte-identical reports."""
+    rng = np.random.default_rng(3)
+    tr = PP.Trace.create(4, 8)
+    for it in range(5):
+        for layer in (0, 1):
+            p = np.arange(1, 9) ** -1.2
+            tr.append(it, layer, np.stack([rng.multinomial(2048, p / p.sum()) for _ in range(4)]))
+    path = tmp_path / "observed.jsonl"
+    tr.save(str(path))
+    assert PP.Trace.load(str(path)).dims() == (4, 8, 10)
+    cfg = json.dumps({"topology": {"n_nodes": 1, "devices_per_node": 4, "b_intra": 9e11, "b_inter": 9e11},
+                      "cost": {"v_comm": 8192, "v_comp": 3.523e8, "b_comp": 1.6354e15},
+                      "model": {"n_experts": 8, "capacity": 4}, "planner": {"seed": 7}})
+    mine = PP.simulate(PP.Config(cfg), PP.Trace.load(str(path)), "laer,static_ep")
+    theirs = ref.simulate(ref.config(cfg), ref.trace_load(str(path)), "laer,static_ep")
+    assert mine == theirs
+    from paper_2602_11686_b200._lib import MoeplanError
+    with pytest.raises(MoeplanError):
+        tr.append(0, 0, np.zeros((4, 8)))  # duplicate (iter, layer)
