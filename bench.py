@@ -180,6 +180,37 @@ def run_reference_impl(args, cfg):
 
 
 # ---------------------------------------------------------------- GPU path
+def token_kernel_bandwidth(phases, layer, PL, N, rank, T, K, H):
+    """HBM and NVLink throughput of the token-movement kernels (rank 0's layer 0).
+
+    Algorithmic bytes per step (bf16 rows of H elements, T tokens, K slots each):
+      dispatch    read x (T*H*2)              + write T*K rows into the owners' arenas
+      combine     read T*K rows (local/peer)   + write y (T*H*2)
+      unpermute   read T*K dx rows (local/peer) + write dx (T*H*2)
+    The remote share (rows whose slot lives on another GPU, i.e. NVLink traffic)
+    comes from lite_routing(R, A) of the step's histogram and layout.
+    """
+    row = H * 2
+    remote = 0
+    if N > 1:
+        R = layer.histogram()
+        A = layer.read("layout").reshape(R.shape[1], N)
+        S = PL.lite_routing(R, A)[rank]  # [E, dst]
+        remote = int(S.sum() - S[:, rank].sum())
+    out = {}
+    for name, ph in (("dispatch", "dispatch"), ("combine", "combine"), ("unpermute", "unpermute")):
+        ms = phases.get(ph) or 0.0
+        if ms <= 0:
+            continue
+        b = T * row + T * K * row
+        out[name] = {"ms": round(ms, 4), "bytes": b, "GBps": round(b / (ms * 1e-3) / 1e9, 1),
+                     "remote_rows": remote, "nvlink_GBps": round(remote * row / (ms * 1e-3) / 1e9, 1)}
+    hbm = peaks()[2]
+    for v in out.values():
+        v["hbm_frac"] = round(v["GBps"] / hbm, 4)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
@@ -195,6 +226,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-static", action="store_true")
+    ap.add_argument("--no-phases", action="store_true", help="skip per-phase device timing events")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.tokens:
@@ -204,6 +236,8 @@ def main():
     if args.impl == "reference":
         return run_reference_impl(args, cfg)
 
+    if not args.no_phases:
+        os.environ.setdefault("FSEP_PHASE_TIMING", "1")
     import torch
     import torch.distributed as dist
 
@@ -308,6 +342,7 @@ def main():
     clocks = clk.result
     sts = [layer.stats() for layer in layers]
     phases = layers[0].phase_ms() if os.environ.get("FSEP_PHASE_TIMING") == "1" else None
+    comm = token_kernel_bandwidth(phases, layers[0], PL, N, rank, T, K, H) if phases else None
     st = {"gemm_ms": sum(s_["gemm_ms"] for s_ in sts), "gemm_flops": sum(s_["gemm_flops"] for s_ in sts),
           "kernel_launches": sum(s_["kernel_launches"] for s_ in sts)}
     value = N * T / (ms * 1e-3)
@@ -419,6 +454,8 @@ def main():
             line["static_ep"] = static
         if phases:
             line["phases_ms_layer0"] = phases
+        if comm:
+            line["token_kernels_layer0"] = comm
         print(json.dumps(line), flush=True)
     for layer in layers:
         layer.close()
