@@ -1,6 +1,7 @@
 // Host launchers for the grouped tcgen05 GEMM (grouped_gemm.cuh) and TMA
 // tensor-map construction (driver entry point fetched through the runtime, so
 // the library does not link libcuda directly).
+#include <cstdlib>
 #include <cudaTypedefs.h>
 
 #include <atomic>
@@ -86,12 +87,12 @@ void launch_pair(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p
   auto kern = grouped_gemm_pair_kernel<AMN, BMN, GK, EPI>;
   static std::once_flag once;
   std::call_once(once, [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm2::SMEM_BYTES);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm2::smem_bytes(EPI));
   });
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(grid & ~1));
   cfg.blockDim = dim3(gemm2::THREADS);
-  cfg.dynamicSmemBytes = gemm2::SMEM_BYTES;
+  cfg.dynamicSmemBytes = gemm2::smem_bytes(EPI);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -116,7 +117,8 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
   if (!pair_gemm_supported(kind, a)) throw std::runtime_error("pair gemm: wgrad M must be a multiple of 256");
   GemmParams p{a.num_groups, a.group_rows, a.group_off, a.M,    a.N,    a.K,   a.out,
                a.ldo,        a.out_group_stride, a.out2,    a.ldo2, a.aux, a.ld_aux, a.policy, a.raster,
-               a.ready,      a.ready_epoch,      a.ready_n};
+               a.ready,      a.ready_epoch,      a.ready_n,
+               a.row_src,    a.scatter,          a.scatter_rows};
   switch (kind) {
     case GemmKind::kFwdGateUp: launch_pair<false, false, false, kEpiSwigluFwd>(tmA, tmB, p, num_sms, stream); break;
     case GemmKind::kFwdDown: launch_pair<false, false, false, kEpiBf16>(tmA, tmB, p, num_sms, stream); break;
@@ -132,7 +134,8 @@ void launch_grouped_gemm(GemmKind kind, const CUtensorMap& tmA, const CUtensorMa
   if (a.N % 32 != 0) throw std::runtime_error("grouped gemm: N must be a multiple of 32");
   GemmParams p{a.num_groups, a.group_rows, a.group_off, a.M,    a.N,    a.K,   a.out,
                a.ldo,        a.out_group_stride, a.out2,    a.ldo2, a.aux, a.ld_aux, a.policy, a.raster,
-               a.ready,      a.ready_epoch,      a.ready_n};
+               a.ready,      a.ready_epoch,      a.ready_n,
+               a.row_src,    a.scatter,          a.scatter_rows};
   switch (kind) {
     case GemmKind::kFwdGateUp: launch_one<false, false, false, kEpiSwigluFwd>(tmA, tmB, p, num_sms, stream); break;
     case GemmKind::kFwdDown: launch_one<false, false, false, kEpiBf16>(tmA, tmB, p, num_sms, stream); break;

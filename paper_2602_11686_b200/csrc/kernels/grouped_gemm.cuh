@@ -54,7 +54,23 @@ struct GemmParams {
   const unsigned* ready;
   unsigned ready_epoch;
   int ready_n;
+  // Optional row scatter (kEpiBf16, M-grouped): output row r is stored to
+  // scatter[code >> 26] + (code & 0x3FFFFFF) * ldo, code = row_src[r] (code < 0:
+  // padding row, not stored).  This is how the expert outputs travel straight
+  // from the GEMM epilogue into the token owner's slot rows over NVLink.
+  const int* row_src;
+  __nv_bfloat16* const* scatter;
+  long long scatter_rows;
 };
+
+__device__ __forceinline__ __nv_bfloat16* bf16_out_row(const GemmParams& p, long long row) {
+  if (p.row_src == nullptr) return static_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
+  const int code = p.row_src[row];
+  if (code < 0) return nullptr;
+  const long long idx = code & 0x3FFFFFF;
+  if (idx >= p.scatter_rows) return nullptr;
+  return p.scatter[code >> 26] + idx * p.ldo;
+}
 
 __device__ __forceinline__ void wait_group_ready(const GemmParams& p, int g) {
   if (p.ready == nullptr) return;
@@ -81,7 +97,10 @@ constexpr int THREADS = 192;
 constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/ + (MAX_GROUPS + 1) * 4;
 }  // namespace gemm
 
-__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+// MUFU-based (approximate reciprocal, ~2 ulp fp32): the result is rounded to bf16, and an
+// IEEE division would cost a slow-path subroutine call per element in the epilogue.
+__device__ __forceinline__ float sigmoid_f(float g) { return __fdividef(1.0f, 1.0f + __expf(-g)); }
+__device__ __forceinline__ float silu_f(float g) { return g * sigmoid_f(g); }
 
 __device__ __forceinline__ uint64_t pick_policy(int code, bool first_by_default) {
   switch (code) {
@@ -307,13 +326,14 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
         }
       } else if (kEpi == kEpiBf16) {
         const long long row = p.group_off[g] + mb * BM + r;
-        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
+        __nv_bfloat16* out = bf16_out_row(p, row);
 #pragma unroll 1
         for (int j = 0; j < BN / 32; ++j) {
           const int col = nbk * BN + j * 32;
           if (col >= p.N) break;
           float v[32];
-          tmem_ld32(taddr + j * 32, v);
+          tmem_ld32(taddr + j * 32, v);  // warp-collective: every lane loads, only live rows store
+          if (out == nullptr) continue;
           uint4* dst = reinterpret_cast<uint4*>(out + col);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
@@ -371,7 +391,7 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
             for (int q = 0; q < 8; ++q) {
               const float gg = __bfloat162float(gb[q]);
               const float uu = __bfloat162float(ub[q]);
-              const float sg = 1.0f / (1.0f + __expf(-gg));
+              const float sg = sigmoid_f(gg);
               const float d = da[8 * i + q];
               du[q] = d * gg * sg;
               dg[q] = d * uu * sg * (1.0f + gg * (1.0f - sg));

@@ -35,6 +35,60 @@ constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 64 + EPI_WARPS * 32;
 constexpr int MAX_GROUPS = 256;
 constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 512 + (MAX_GROUPS + 1) * 4;
+// SwiGLU-bwd epilogue: per-warp [32 rows][32 fp32] transpose tile (XOR-swizzled float4 slots)
+constexpr int EPI_STAGE_OFF = (STAGES * STAGE_BYTES + 512 + (MAX_GROUPS + 1) * 4 + 127) / 128 * 128;
+constexpr int EPI_STAGE_BYTES = EPI_WARPS * 32 * 32 * 4;
+// bf16 epilogues: per-warp [32 rows][64 B] row-piece transpose tile
+constexpr int EPI_STAGE16_BYTES = EPI_WARPS * 32 * 64;
+constexpr int smem_bytes(int epi) {
+  return epi == kEpiSwigluBwd ? 1024 + EPI_STAGE_OFF + EPI_STAGE_BYTES
+                              : (epi == kEpiF32 ? SMEM_BYTES : 1024 + EPI_STAGE_OFF + EPI_STAGE16_BYTES);
+}
+static_assert(1024 + EPI_STAGE_OFF + EPI_STAGE_BYTES <= 232448, "SwiGLU-bwd staging exceeds shared memory");
+
+// Coalesced store of a warp's 32 row pieces of 64 B (32 bf16): lane r holds row
+// r's piece in v[0..3]; the pieces are transposed through a 2 KB smem tile
+// (XOR-swizzled 16-B slots, conflict-free both ways) so that every store
+// instruction writes 8 rows x 64 contiguous bytes instead of 32 scattered 16-B
+// pieces.  dst(rr) gives row rr's destination (nullptr: row not stored).
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
+
+// Coalesced store of a warp's 32 row pieces of 64 B (32 bf16): lane r holds row
+// r's piece in v[0..3]; the pieces are transposed through a 2 KB smem tile
+// (XOR-swizzled 16-B slots, conflict-free both ways) so that every store
+// instruction writes 8 rows x 64 contiguous bytes instead of 32 scattered 16-B
+// pieces.  dst(rr) gives row rr's destination (nullptr: row not stored).
+template <typename Dst>
+__device__ __forceinline__ void warp_store_rows64(uint32_t stg, const uint4 (&v)[4], Dst dst) {
+  const int lane = static_cast<int>(threadIdx.x & 31);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) sts128(stg + 16 * (lane * 4 + (q ^ ((lane >> 1) & 3))), v[q]);
+  __syncwarp();
+  const int sub = lane >> 2, cg = lane & 3;
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int rr = it * 8 + sub;
+    const uint4 x = lds128(stg + 16 * (rr * 4 + (cg ^ ((rr >> 1) & 3))));
+    __nv_bfloat16* d = dst(rr);
+    if (d != nullptr) reinterpret_cast<uint4*>(d)[cg] = x;
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void pack_row64(const float* v, uint4 (&o)[4]) {
+  using ptx::pack_bf16;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    o[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                      pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+}
 }  // namespace gemm2
 
 template <bool kAMN, bool kBMN, bool kGroupK, int kEpi>
@@ -239,8 +293,9 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
             for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
           }
         } else if (kEpi == kEpiBf16) {
+          const uint32_t stg = ptx::smem_u32(smem + EPI_STAGE_OFF) + (warp - 2) * 2048;
           const long long row = p.group_off[g] + m_half + r;
-          __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
+          __nv_bfloat16* out = bf16_out_row(p, row);  // own row (row scatter resolved per lane)
 #pragma unroll 1
           for (int j = 0; j < 4; ++j) {
             const int c = half * 128 + j * 32;
@@ -248,96 +303,104 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
             if (col >= p.N) break;
             float v[32];
             tmem_ld32(taddr + c, v);
-            uint4* dst = reinterpret_cast<uint4*>(out + col);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              dst[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                                  pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+            uint4 o[4];
+            pack_row64(v, o);
+            warp_store_rows64(stg, o, [&](int rr) {
+              __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(
+                  __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(out), rr));
+              return d == nullptr ? d : d + col;
+            });
           }
         } else if (kEpi == kEpiSwigluFwd) {
           // tile columns [0,128) = gate f0.., [128,256) = up f0..; this warp: f in [64*half, 64*half+64)
-          const long long row = p.group_off[g] + m_half + r;
-          __nv_bfloat16* h = static_cast<__nv_bfloat16*>(p.out) + row * p.ldo + nbk * BN;
-          __nv_bfloat16* act = static_cast<__nv_bfloat16*>(p.out2) + row * p.ldo2 + nbk * (BN / 2);
+          const uint32_t stg = ptx::smem_u32(smem + EPI_STAGE_OFF) + (warp - 2) * 2048;
+          const long long row0 = p.group_off[g] + m_half + quarter * 32;
+          __nv_bfloat16* hb = static_cast<__nv_bfloat16*>(p.out) + nbk * BN;
+          __nv_bfloat16* ab = static_cast<__nv_bfloat16*>(p.out2) + nbk * (BN / 2);
 #pragma unroll 1
           for (int j = 0; j < 2; ++j) {
             const int f = half * 64 + j * 32;
             float gv[32], uv[32];
             tmem_ld32(taddr + f, gv);
             tmem_ld32(taddr + 128 + f, uv);
-            uint4* hg = reinterpret_cast<uint4*>(h + f);
-            uint4* hu = reinterpret_cast<uint4*>(h + 128 + f);
-            uint4* ao = reinterpret_cast<uint4*>(act + f);
+            uint4 o[4];
+            pack_row64(gv, o);
+            warp_store_rows64(stg, o, [&](int rr) { return hb + (row0 + rr) * p.ldo + f; });
+            pack_row64(uv, o);
+            warp_store_rows64(stg, o, [&](int rr) { return hb + (row0 + rr) * p.ldo + 128 + f; });
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              hg[i] = make_uint4(pack_bf16(gv[8 * i], gv[8 * i + 1]), pack_bf16(gv[8 * i + 2], gv[8 * i + 3]),
-                                 pack_bf16(gv[8 * i + 4], gv[8 * i + 5]), pack_bf16(gv[8 * i + 6], gv[8 * i + 7]));
-              hu[i] = make_uint4(pack_bf16(uv[8 * i], uv[8 * i + 1]), pack_bf16(uv[8 * i + 2], uv[8 * i + 3]),
-                                 pack_bf16(uv[8 * i + 4], uv[8 * i + 5]), pack_bf16(uv[8 * i + 6], uv[8 * i + 7]));
-              float a[8];
-#pragma unroll
-              for (int q = 0; q < 8; ++q) a[q] = silu_f(gv[8 * i + q]) * uv[8 * i + q];
-              ao[i] = make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]),
-                                 pack_bf16(a[6], a[7]));
-            }
+            for (int q = 0; q < 32; ++q) gv[q] = silu_f(gv[q]) * uv[q];
+            pack_row64(gv, o);
+            warp_store_rows64(stg, o, [&](int rr) { return ab + (row0 + rr) * p.ldo2 + f; });
           }
-        } else {  // kEpiSwigluBwd: software-pipelined h loads (chunk j+1 in flight while j computes)
-          const long long row = p.group_off[g] + m_half + r;
-          const __nv_bfloat16* h = static_cast<const __nv_bfloat16*>(p.aux) + row * p.ld_aux;
-          __nv_bfloat16* dh = static_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
-          int nchunks = 0;
+        } else {  // kEpiSwigluBwd
+          // dAct arrives one row per lane (TMEM 32x32b); it is transposed through a
+          // per-warp smem tile so that the h loads and dH stores are row-contiguous
+          // across lanes (4 lanes x 16 B of one row, 8 rows per instruction) rather
+          // than one 16-B piece of 32 different rows per instruction.  The h loads
+          // of chunk j+1 are in flight while chunk j computes.
+          const uint32_t stg = ptx::smem_u32(smem + EPI_STAGE_OFF) + (warp - 2) * 4096;
+          const long long row0 = p.group_off[g] + m_half + quarter * 32;
+          const int sub = static_cast<int>(lane >> 2), cg = static_cast<int>(lane & 3);
+          const __nv_bfloat16* hb = static_cast<const __nv_bfloat16*>(p.aux);
+          __nv_bfloat16* db = static_cast<__nv_bfloat16*>(p.out);
+          int nch = 0;
           for (int j = 0; j < 4; ++j)
-            if (nbk * BN + half * 128 + j * 32 < p.N) nchunks = j + 1;
-          auto hcol_of = [&](int j) {
+            if (nbk * BN + half * 128 + j * 32 < p.N) nch = j + 1;
+          auto hcol = [&](int j) {
             const int f = nbk * BN + half * 128 + j * 32;
-            return (f / 128) * 256 + (f % 128);
+            return static_cast<long long>((f / 128) * 256 + (f % 128) + cg * 8);
+          };
+          auto load_h = [&](int j, uint4 (&gq)[4], uint4 (&uq)[4]) {
+            const long long hc = hcol(j);
+#pragma unroll
+            for (int it = 0; it < 4; ++it) {
+              const __nv_bfloat16* hr = hb + (row0 + it * 8 + sub) * p.ld_aux + hc;
+              gq[it] = *reinterpret_cast<const uint4*>(hr);
+              uq[it] = *reinterpret_cast<const uint4*>(hr + 128);
+            }
           };
           uint4 gq[4], uq[4];
-          if (nchunks > 0) {
-            const uint4* g4 = reinterpret_cast<const uint4*>(h + hcol_of(0));
-            const uint4* u4 = reinterpret_cast<const uint4*>(h + hcol_of(0) + 128);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              gq[i] = g4[i];
-              uq[i] = u4[i];
-            }
-          }
+          if (nch > 0) load_h(0, gq, uq);
 #pragma unroll 1
-          for (int j = 0; j < nchunks; ++j) {
-            uint4 gn[4], un[4];
-            if (j + 1 < nchunks) {
-              const uint4* g4 = reinterpret_cast<const uint4*>(h + hcol_of(j + 1));
-              const uint4* u4 = reinterpret_cast<const uint4*>(h + hcol_of(j + 1) + 128);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                gn[i] = g4[i];
-                un[i] = u4[i];
-              }
-            }
+          for (int j = 0; j < nch; ++j) {
             float da[32];
             tmem_ld32(taddr + half * 128 + j * 32, da);
-            const int hc = hcol_of(j);
-            uint4* dg4 = reinterpret_cast<uint4*>(dh + hc);
-            uint4* du4 = reinterpret_cast<uint4*>(dh + hc + 128);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const __nv_bfloat16* gb = reinterpret_cast<const __nv_bfloat16*>(&gq[i]);
-              const __nv_bfloat16* ub = reinterpret_cast<const __nv_bfloat16*>(&uq[i]);
+            for (int q = 0; q < 8; ++q)
+              sts128(stg + 16 * (lane * 8 + (q ^ (lane & 7))),
+                     make_uint4(__float_as_uint(da[4 * q]), __float_as_uint(da[4 * q + 1]),
+                                __float_as_uint(da[4 * q + 2]), __float_as_uint(da[4 * q + 3])));
+            uint4 gn[4], un[4];
+            if (j + 1 < nch) load_h(j + 1, gn, un);
+            __syncwarp();
+            const long long hc = hcol(j);
+#pragma unroll
+            for (int it = 0; it < 4; ++it) {
+              const int rr = it * 8 + sub;
+              const uint4 d0 = lds128(stg + 16 * (rr * 8 + ((2 * cg) ^ (rr & 7))));
+              const uint4 d1 = lds128(stg + 16 * (rr * 8 + ((2 * cg + 1) ^ (rr & 7))));
+              const float d[8] = {__uint_as_float(d0.x), __uint_as_float(d0.y), __uint_as_float(d0.z),
+                                  __uint_as_float(d0.w), __uint_as_float(d1.x), __uint_as_float(d1.y),
+                                  __uint_as_float(d1.z), __uint_as_float(d1.w)};
+              const __nv_bfloat16* gb = reinterpret_cast<const __nv_bfloat16*>(&gq[it]);
+              const __nv_bfloat16* ub = reinterpret_cast<const __nv_bfloat16*>(&uq[it]);
               float dg[8], du[8];
 #pragma unroll
               for (int q = 0; q < 8; ++q) {
                 const float gg = __bfloat162float(gb[q]);
                 const float uu = __bfloat162float(ub[q]);
-                const float sg = 1.0f / (1.0f + __expf(-gg));
-                const float d = da[8 * i + q];
-                du[q] = d * gg * sg;
-                dg[q] = d * uu * sg * (1.0f + gg * (1.0f - sg));
+                const float sg = sigmoid_f(gg);
+                du[q] = d[q] * gg * sg;
+                dg[q] = d[q] * uu * sg * (1.0f + gg * (1.0f - sg));
               }
-              dg4[i] = make_uint4(pack_bf16(dg[0], dg[1]), pack_bf16(dg[2], dg[3]), pack_bf16(dg[4], dg[5]),
-                                  pack_bf16(dg[6], dg[7]));
-              du4[i] = make_uint4(pack_bf16(du[0], du[1]), pack_bf16(du[2], du[3]), pack_bf16(du[4], du[5]),
-                                  pack_bf16(du[6], du[7]));
+              __nv_bfloat16* dr = db + (row0 + rr) * p.ldo + hc;
+              *reinterpret_cast<uint4*>(dr) = make_uint4(pack_bf16(dg[0], dg[1]), pack_bf16(dg[2], dg[3]),
+                                                         pack_bf16(dg[4], dg[5]), pack_bf16(dg[6], dg[7]));
+              *reinterpret_cast<uint4*>(dr + 128) = make_uint4(pack_bf16(du[0], du[1]), pack_bf16(du[2], du[3]),
+                                                               pack_bf16(du[4], du[5]), pack_bf16(du[6], du[7]));
             }
+            __syncwarp();
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               gq[i] = gn[i];

@@ -2,6 +2,7 @@
 // C ABI).  Every launcher is asynchronous on the given stream.
 #pragma once
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -34,6 +35,9 @@ struct GroupedGemmArgs {
   const unsigned* ready = nullptr;  // per-group readiness flags (see GemmParams)
   unsigned ready_epoch = 0;
   int ready_n = 0;
+  const int* row_src = nullptr;  // optional row scatter of the bf16 epilogue (see GemmParams)
+  __nv_bfloat16* const* scatter = nullptr;
+  long long scatter_rows = 0;
 };
 
 enum class GemmKind : int {

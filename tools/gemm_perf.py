@@ -9,13 +9,33 @@ _knobs = (int(os.environ.get('POL', '0')) << 12) | (int(os.environ.get('RASTER',
 TG.KINDS = {k: v | _knobs for k, v in TG.KINDS.items()}
 _run = functools.partial(_run0, pair=os.environ.get('PAIR', '1') == '1', sync=False)
 
-def bench(fn, iters=10):
+import threading
+try:
+    import pynvml
+    pynvml.nvmlInit()
+    _nv = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+except Exception:
+    _nv = None
+
+
+def bench(fn, iters=30):
+    """Mean ms per call, and the mean SM clock (MHz) sampled while the calls ran."""
     for _ in range(3): fn()
     torch.cuda.synchronize()
+    clk, stop = [], threading.Event()
+
+    def sample():
+        while not stop.is_set():
+            if _nv is not None:
+                clk.append(pynvml.nvmlDeviceGetClockInfo(_nv, pynvml.NVML_CLOCK_SM))
+            stop.wait(0.005)
+    th = threading.Thread(target=sample); th.start()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for _ in range(iters): fn()
     e.record(); torch.cuda.synchronize()
+    stop.set(); th.join()
+    bench.mhz = sum(clk) / len(clk) if clk else float("nan")
     return s.elapsed_time(e) / iters
 
 H, F, G, rows = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
@@ -36,9 +56,16 @@ tests = {
  "wgrad_w2": (lambda: _run("wgrad", G, rg, off, H, F, 0, dY, R, H, act, F, R, 1, F, 0, gW2, F, ogs=H*F), 2*R*H*F),
  "wgrad_w13": (lambda: _run("wgrad", G, rg, off, 2*F, H, 0, dH, R, 2*F, X, H, R, 1, H, 0, gW13, H, ogs=2*F*H), 2*R*H*2*F),
 }
+if os.environ.get("PLAIN") == "1":  # same shapes as the SwiGLU kernels, plain bf16 epilogue
+    dA = torch.empty(R, F, device="cuda", dtype=torch.bfloat16)
+    tests["gateup_plain"] = (lambda: _run("down", G, rg, off, 0, 2*F, H, X, R, H, W13, H, 2*F, G, H, 2*F*H, h, 2*F), 2*R*H*2*F)
+    tests["down_dgrad_plain"] = (lambda: _run("up_dgrad", G, rg, off, 0, F, H, dY, R, H, W2, F, H, G, F, H*F, dA, F), 2*R*H*F)
+if os.environ.get("ONLY"):
+    tests = {k: v for k, v in tests.items() if k in os.environ["ONLY"].split(",")}
 tot_ms = tot_fl = 0
 for name, (fn, fl) in tests.items():
     ms = bench(fn)
     tot_ms += ms; tot_fl += fl
-    print(f"{name:12s} {ms:8.3f} ms  {fl/ms/1e9:8.1f} TFLOP/s")
+    eff = fl / (ms * 1e-3) / (148 * 8192 * bench.mhz * 1e6)
+    print(f"{name:16s} {ms:8.3f} ms  {fl/ms/1e9:8.1f} TFLOP/s  sm {bench.mhz:6.0f} MHz  per-clock {100*eff:5.1f}%")
 print(f"total {tot_ms:.3f} ms {tot_fl/tot_ms/1e9:.1f} TFLOP/s")
