@@ -23,11 +23,16 @@ constexpr int kBlockTokens = 64;  // router / ranking tile (8 warps x 8 tokens)
 constexpr int kDLCols = 128;      // width of the dense router-gradient matrix dL[t][e] (>= E)
 constexpr int kRouterWgradChunk = 1024;  // token rows per split-K group of the router wgrad GEMM
 
+// Token-slot rows: every rank owns tok_rows[T_max * K][H] indexed by its own
+// (token, k) slot.  The expert GEMMs' epilogues store their output rows (y in
+// the forward, dX in the backward) straight into the owner's tok_rows over
+// NVLink, guided by row_src, so combine / unpermute read only local HBM.
+constexpr int kRowSrcShift = 26;  // row_src code = (source rank << 26) | (t * K + k); -1 = padding row
 struct PeerTable {
   __nv_bfloat16* x_rows[kMaxRanks];
-  __nv_bfloat16* y_rows[kMaxRanks];
   __nv_bfloat16* dy_rows[kMaxRanks];
-  __nv_bfloat16* dx_rows[kMaxRanks];
+  __nv_bfloat16* tok_rows[kMaxRanks];  // [T_max*K][H] on each rank (y, later reused for dX)
+  int* row_src[kMaxRanks];             // [row_capacity] origin of each receive row on each rank
   unsigned long long* R_all[kMaxRanks];  // [N][E] on each rank
   float* grad_full[kMaxRanks];           // [C][3HF] restored-expert grads on each rank
   const __nv_bfloat16* shard[kMaxRanks]; // [E][S] FSEP shards on each rank

@@ -126,10 +126,11 @@ __global__ void plan_kernel(const unsigned long long* __restrict__ R_all, const 
 // Zero the padding rows of this rank's receive buffers (X rows and dY rows) so
 // the GEMMs may run over padded segments and the wgrad reduction stays exact.
 __global__ void zero_pad_kernel(const PlanTables* __restrict__ pt, int C, int H, __nv_bfloat16* x_rows,
-                                __nv_bfloat16* dy_rows) {
+                                __nv_bfloat16* dy_rows, int* row_src) {
   const int c = blockIdx.y;
   if (c >= C) return;
   const int rows = pt->seg_rows[c], pad = pt->seg_rows_pad[c] - rows;
+  if (blockIdx.x == 0 && static_cast<int>(threadIdx.x) < pad) row_src[pt->seg_off[c] + rows + threadIdx.x] = -1;
   const size_t base = static_cast<size_t>(pt->seg_off[c] + rows) * H;
   const size_t n = static_cast<size_t>(pad) * H / 8;
   uint4 z = make_uint4(0, 0, 0, 0);
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
                                                        const int* __restrict__ intra_rank,
                                                        const int* __restrict__ blk_base,
                                                        const PlanTables* __restrict__ pt, PeerTable peers,
-                                                       uint32_t* __restrict__ slot_dst) {
+                                                       uint32_t* __restrict__ slot_dst, int src_rank) {
   constexpr int H = CH * 256;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -161,10 +162,12 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
     while (pt->src_cum[e][h + 1] <= r) ++h;
     const int d = pt->host_dev[e][h];
     const long long row = pt->src_row_base[e][h] + (r - pt->src_cum[e][h]);
-    if (lane == 0) slot_dst[static_cast<size_t>(t) * K + k] = (static_cast<uint32_t>(d) << 24) | static_cast<uint32_t>(row);
-    dst_row[k] = (static_cast<uint64_t>(row) < peers.row_capacity)
-                     ? reinterpret_cast<uint4*>(peers.x_rows[d] + static_cast<size_t>(row) * H)
-                     : nullptr;
+    const bool fits = static_cast<uint64_t>(row) < peers.row_capacity;
+    if (lane == 0) {
+      slot_dst[static_cast<size_t>(t) * K + k] = (static_cast<uint32_t>(d) << 24) | static_cast<uint32_t>(row);
+      if (fits) peers.row_src[d][row] = (src_rank << kRowSrcShift) | (t * K + k);
+    }
+    dst_row[k] = fits ? reinterpret_cast<uint4*>(peers.x_rows[d] + static_cast<size_t>(row) * H) : nullptr;
   }
   const uint4* src = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * H);
   uint4 v[CH];
@@ -185,7 +188,7 @@ __device__ __forceinline__ const uint4* row_ptr(__nv_bfloat16* const* bufs, uint
 // out[t] = sum_k w[t,k] * y[slot(t,k)]  (fp32 accumulate in k order, bf16 out)
 template <int CH>
 __global__ void __launch_bounds__(256) combine_kernel(int T, int K, const float* __restrict__ topk_w,
-                                                      const uint32_t* __restrict__ slot_dst, PeerTable peers,
+                                                      const __nv_bfloat16* __restrict__ tok_rows,
                                                       __nv_bfloat16* __restrict__ out) {
   constexpr int H = CH * 256;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -201,7 +204,7 @@ __global__ void __launch_bounds__(256) combine_kernel(int T, int K, const float*
       for (int j = 0; j < 8; ++j) acc[c][j] = 0.f;
     for (int k = 0; k < K; ++k) {
       const float w = topk_w[static_cast<size_t>(t) * K + k];
-      const uint4* y = row_ptr(peers.y_rows, slot_dst[static_cast<size_t>(t) * K + k], H);
+      const uint4* y = reinterpret_cast<const uint4*>(tok_rows + (static_cast<size_t>(t) * K + k) * H);
       uint4 q[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
@@ -232,6 +235,7 @@ template <int CH>
 __global__ void __launch_bounds__(256) combine_bwd_kernel(int T, int K, const __nv_bfloat16* __restrict__ dout,
                                                           const float* __restrict__ topk_w,
                                                           const int* __restrict__ topk_idx,
+                                                          const __nv_bfloat16* __restrict__ tok_rows,
                                                           const uint32_t* __restrict__ slot_dst, PeerTable peers,
                                                           float* __restrict__ dl, __nv_bfloat16* __restrict__ dl_dense,
                                                           int* __restrict__ rw_rows, int* __restrict__ rw_off) {
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(int T, int K, const __
       if (c0 + c < CH) bf16x8_to_f32(__ldg(g + (c0 + c) * 32 + lane), gf[c]);
     for (int k = 0; k < K; ++k) {
       const uint32_t code = slot_dst[static_cast<size_t>(t) * K + k];
-      const uint4* y = row_ptr(peers.y_rows, code, H);
+      const uint4* y = reinterpret_cast<const uint4*>(tok_rows + (static_cast<size_t>(t) * K + k) * H);
       uint4* dy = const_cast<uint4*>(row_ptr(peers.dy_rows, code, H));
       uint4 q[4];
 #pragma unroll
@@ -300,8 +304,8 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(int T, int K, const __
 template <int CH>
 __global__ void __launch_bounds__(256) unpermute_bwd_kernel(int T, int K, const int* __restrict__ topk_idx,
                                                             const float* __restrict__ dl,
-                                                            const uint32_t* __restrict__ slot_dst,
-                                                            const __nv_bfloat16* __restrict__ wg, PeerTable peers,
+                                                            const __nv_bfloat16* __restrict__ tok_rows,
+                                                            const __nv_bfloat16* __restrict__ wg,
                                                             __nv_bfloat16* __restrict__ dx) {
   constexpr int H = CH * 256;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -316,7 +320,7 @@ __global__ void __launch_bounds__(256) unpermute_bwd_kernel(int T, int K, const 
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[c][j] = 0.f;
     for (int k = 0; k < K; ++k) {
-      const uint4* r = row_ptr(peers.dx_rows, slot_dst[static_cast<size_t>(t) * K + k], H);
+      const uint4* r = reinterpret_cast<const uint4*>(tok_rows + (static_cast<size_t>(t) * K + k) * H);
       const float d = dl[static_cast<size_t>(t) * K + k];
       const uint4* w = reinterpret_cast<const uint4*>(wg + static_cast<size_t>(topk_idx[static_cast<size_t>(t) * K + k]) * H);
 #pragma unroll
@@ -483,42 +487,42 @@ void launch_plan(const unsigned long long* R_all, const uint8_t* layout, int E, 
   count_launch();
 }
 
-void launch_zero_pad(const PlanTables* pt, int C, int H, __nv_bfloat16* x_rows, __nv_bfloat16* dy_rows,
+void launch_zero_pad(const PlanTables* pt, int C, int H, __nv_bfloat16* x_rows, __nv_bfloat16* dy_rows, int* row_src,
                      cudaStream_t st) {
-  zero_pad_kernel<<<dim3(16, C), 256, 0, st>>>(pt, C, H, x_rows, dy_rows);
+  zero_pad_kernel<<<dim3(16, C), 256, 0, st>>>(pt, C, H, x_rows, dy_rows, row_src);
   count_launch();
 }
 
 void launch_dispatch(const DispatchArgs& a, cudaStream_t st) {
   if (a.T == 0) return;
   FSEP_CH_SWITCH(a.H / 256, dispatch_kernel<CH><<<(a.T + 7) / 8, 256, 0, st>>>(
-                                a.x, a.T, a.K, a.E, a.topk_idx, a.intra_rank, a.blk_base, a.pt, a.peers, a.slot_dst));
+                                a.x, a.T, a.K, a.E, a.topk_idx, a.intra_rank, a.blk_base, a.pt, a.peers, a.slot_dst,
+                                a.rank));
   count_launch();
 }
 
-void launch_combine(int T, int H, int K, const float* topk_w, const uint32_t* slot_dst, const PeerTable& peers,
-                    __nv_bfloat16* out, cudaStream_t st) {
+void launch_combine(int T, int H, int K, const float* topk_w, const __nv_bfloat16* tok_rows, __nv_bfloat16* out,
+                    cudaStream_t st) {
   if (T == 0) return;
-  FSEP_CH_SWITCH(H / 256, combine_kernel<CH><<<(T + 7) / 8, 256, 0, st>>>(T, K, topk_w, slot_dst, peers, out));
+  FSEP_CH_SWITCH(H / 256, combine_kernel<CH><<<(T + 7) / 8, 256, 0, st>>>(T, K, topk_w, tok_rows, out));
   count_launch();
 }
 
 void launch_combine_bwd(int T, int H, int K, const __nv_bfloat16* dout, const float* topk_w, const int* topk_idx,
-                        const uint32_t* slot_dst, const PeerTable& peers, float* dl, __nv_bfloat16* dl_dense,
-                        int* rw_rows, int* rw_off, cudaStream_t st) {
+                        const __nv_bfloat16* tok_rows, const uint32_t* slot_dst, const PeerTable& peers, float* dl,
+                        __nv_bfloat16* dl_dense, int* rw_rows, int* rw_off, cudaStream_t st) {
   if (T == 0) return;
   const size_t tpad = (static_cast<size_t>(T) + 127) / 128 * 128;
   cudaMemsetAsync(dl_dense, 0, tpad * kDLCols * sizeof(__nv_bfloat16), st);
-  FSEP_CH_SWITCH(H / 256, combine_bwd_kernel<CH><<<(T + 7) / 8, 256, 0, st>>>(T, K, dout, topk_w, topk_idx, slot_dst,
-                                                                               peers, dl, dl_dense, rw_rows, rw_off));
+  FSEP_CH_SWITCH(H / 256, combine_bwd_kernel<CH><<<(T + 7) / 8, 256, 0, st>>>(
+                              T, K, dout, topk_w, topk_idx, tok_rows, slot_dst, peers, dl, dl_dense, rw_rows, rw_off));
   count_launch();
 }
 
-void launch_unpermute_bwd(int T, int H, int K, const int* topk_idx, const float* dl, const uint32_t* slot_dst,
-                          const __nv_bfloat16* wg, const PeerTable& peers, __nv_bfloat16* dx, cudaStream_t st) {
+void launch_unpermute_bwd(int T, int H, int K, const int* topk_idx, const float* dl, const __nv_bfloat16* tok_rows,
+                          const __nv_bfloat16* wg, __nv_bfloat16* dx, cudaStream_t st) {
   if (T == 0) return;
-  FSEP_CH_SWITCH(H / 256, unpermute_bwd_kernel<CH><<<(T + 7) / 8, 256, 0, st>>>(T, K, topk_idx, dl, slot_dst, wg,
-                                                                                 peers, dx));
+  FSEP_CH_SWITCH(H / 256, unpermute_bwd_kernel<CH><<<(T + 7) / 8, 256, 0, st>>>(T, K, topk_idx, dl, tok_rows, wg, dx));
   count_launch();
 }
 

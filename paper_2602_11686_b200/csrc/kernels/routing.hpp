@@ -29,6 +29,7 @@ struct DispatchArgs {
   const PlanTables* pt;
   PeerTable peers;
   uint32_t* slot_dst;
+  int rank;  // source rank (row_src codes)
 };
 
 void launch_router(const RouterArgs& a, cudaStream_t st);
@@ -37,15 +38,15 @@ void launch_block_scan(const int* blk_hist, int nblk, int E, int* blk_base, cons
 void launch_plan(const unsigned long long* R_all, const uint8_t* layout, int E, int N, int rank, PlanTables* pt,
                  long long row_capacity, cudaStream_t st);
 void launch_zero_pad(const PlanTables* pt, int C, int H, __nv_bfloat16* x_rows, __nv_bfloat16* dy_rows,
-                     cudaStream_t st);
+                     int* row_src, cudaStream_t st);
 void launch_dispatch(const DispatchArgs& a, cudaStream_t st);
-void launch_combine(int T, int H, int K, const float* topk_w, const uint32_t* slot_dst, const PeerTable& peers,
-                    __nv_bfloat16* out, cudaStream_t st);
+void launch_combine(int T, int H, int K, const float* topk_w, const __nv_bfloat16* tok_rows, __nv_bfloat16* out,
+                    cudaStream_t st);
 void launch_combine_bwd(int T, int H, int K, const __nv_bfloat16* dout, const float* topk_w, const int* topk_idx,
-                        const uint32_t* slot_dst, const PeerTable& peers, float* dl, __nv_bfloat16* dl_dense,
-                        int* rw_rows, int* rw_off, cudaStream_t st);
-void launch_unpermute_bwd(int T, int H, int K, const int* topk_idx, const float* dl, const uint32_t* slot_dst,
-                          const __nv_bfloat16* wg, const PeerTable& peers, __nv_bfloat16* dx, cudaStream_t st);
+                        const __nv_bfloat16* tok_rows, const uint32_t* slot_dst, const PeerTable& peers, float* dl,
+                        __nv_bfloat16* dl_dense, int* rw_rows, int* rw_off, cudaStream_t st);
+void launch_unpermute_bwd(int T, int H, int K, const int* topk_idx, const float* dl, const __nv_bfloat16* tok_rows,
+                          const __nv_bfloat16* wg, __nv_bfloat16* dx, cudaStream_t st);
 int router_wgrad_splits(int T);
 void launch_router_wgrad(const __nv_bfloat16* x, int T, int H, int E, const __nv_bfloat16* dl_dense, int T_max,
                          const int* rw_rows, const int* rw_off, float* partial, float* dwg, int num_sms,

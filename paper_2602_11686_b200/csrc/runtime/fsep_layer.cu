@@ -69,7 +69,8 @@ struct Rank {
   // peer-visible arena
   void* arena = nullptr;
   size_t arena_bytes = 0;
-  __nv_bfloat16 *x_rows = nullptr, *y_rows = nullptr, *dy_rows = nullptr, *dx_rows = nullptr;
+  __nv_bfloat16 *x_rows = nullptr, *dy_rows = nullptr, *tok_rows = nullptr;
+  int* row_src = nullptr;
   unsigned long long* R_all = nullptr;
   float* grad_full = nullptr;
   __nv_bfloat16* shard = nullptr;
@@ -111,6 +112,7 @@ extern "C" struct mp_fsep_layer {
   std::vector<Rank> ranks;  // local ranks (N in virtual mode, 1 in real mode)
   PeerTable peers{};
   unsigned int** d_peer_flags = nullptr;
+  __nv_bfloat16** d_tok_table = nullptr;  // [kMaxRanks] every rank's tok_rows (GEMM epilogue scatter)
   std::vector<cudaIpcMemHandle_t> opened;  // for bookkeeping
   std::vector<void*> opened_ptrs;
   bool connected = false;
@@ -239,9 +241,9 @@ void allocate_rank(Layer& L, Rank& r) {
   size_t a = 0;
   auto acc = [&](size_t bytes) { a = align_up(a, 256) + bytes; };
   acc(cap * H * 2);  // x_rows
-  acc(cap * H * 2);  // y_rows
   acc(cap * H * 2);  // dy_rows
-  acc(cap * H * 2);  // dx_rows
+  acc(T * K * H * 2);  // tok_rows
+  acc(cap * 4);      // row_src
   acc(N * E * 8);    // R_all
   acc(C * flat * 4);  // grad_full
   acc(E * S * 2);    // shard
@@ -251,9 +253,9 @@ void allocate_rank(Layer& L, Rank& r) {
   CK(cudaMemset(r.arena, 0, r.arena_bytes));
   Carver ca{static_cast<char*>(r.arena)};
   r.x_rows = ca.take<__nv_bfloat16>(cap * H);
-  r.y_rows = ca.take<__nv_bfloat16>(cap * H);
   r.dy_rows = ca.take<__nv_bfloat16>(cap * H);
-  r.dx_rows = ca.take<__nv_bfloat16>(cap * H);
+  r.tok_rows = ca.take<__nv_bfloat16>(T * K * H);
+  r.row_src = ca.take<int>(cap);
   r.R_all = ca.take<unsigned long long>(N * E);
   r.grad_full = ca.take<float>(C * flat);
   r.shard = ca.take<__nv_bfloat16>(E * S);
@@ -316,9 +318,9 @@ void finish_peers(Layer& L) {
     for (int p = 0; p < L.N; ++p) {
       Rank& r = L.ranks[p];
       L.peers.x_rows[p] = r.x_rows;
-      L.peers.y_rows[p] = r.y_rows;
       L.peers.dy_rows[p] = r.dy_rows;
-      L.peers.dx_rows[p] = r.dx_rows;
+      L.peers.tok_rows[p] = r.tok_rows;
+      L.peers.row_src[p] = r.row_src;
       L.peers.R_all[p] = r.R_all;
       L.peers.grad_full[p] = r.grad_full;
       L.peers.shard[p] = r.shard;
@@ -428,7 +430,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   // 4. device lite routing + receive layout; dispatch
   for (Rank& r : L.ranks) {
     launch_plan(r.R_all, r.layout_dev, E, N, r.rank, r.pt, L.cap, st);
-    launch_zero_pad(r.pt, C, H, r.x_rows, r.dy_rows, st);
+    launch_zero_pad(r.pt, C, H, r.x_rows, r.dy_rows, r.row_src, st);
   }
   mark(L, st, kPhPlan);
   // histogram -> host planner (async, off the critical path)
@@ -448,7 +450,9 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
     L.planner_pending = true;
   }
   for (Rank& r : L.ranks)
-    launch_dispatch(DispatchArgs{r.x_in, T, H, K, E, r.topk_idx, r.intra_rank, r.blk_base, r.pt, L.peers, r.slot_dst}, st);
+    launch_dispatch(DispatchArgs{r.x_in, T, H, K, E, r.topk_idx, r.intra_rank, r.blk_base, r.pt, L.peers, r.slot_dst,
+                                 r.rank},
+                    st);
   mark(L, st, kPhDispatch);
   barrier(L, st);
   mark(L, st, kPhDispatchBarrier);
@@ -473,8 +477,11 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
     GroupedGemmArgs g2 = g;
     g2.N = H;
     g2.K = F;
-    g2.out = r.y_rows;
+    g2.out = nullptr;  // rows go straight to the token owners' tok_rows (epilogue scatter)
     g2.ldo = H;
+    g2.row_src = r.row_src;
+    g2.scatter = L.d_tok_table;
+    g2.scatter_rows = static_cast<long long>(L.T_max) * K;
     g2.out2 = nullptr;
     g2.ldo2 = 0;
     gemm(L, GemmKind::kFwdDown, r.tm_act_k, r.tm_w2_k, r.tm_w2_k128, g2, st);
@@ -490,7 +497,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   // 6. combine
   for (size_t v = 0; v < L.ranks.size(); ++v) {
     Rank& r = L.ranks[v];
-    launch_combine(T, H, K, r.topk_w, r.slot_dst, L.peers, y + (L.virt ? static_cast<long long>(v) * TH : 0), st);
+    launch_combine(T, H, K, r.topk_w, r.tok_rows, y + (L.virt ? static_cast<long long>(v) * TH : 0), st);
   }
   mark(L, st, kPhCombine);
 }
@@ -500,8 +507,8 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   const long long TH = static_cast<long long>(T) * H;
   for (size_t v = 0; v < L.ranks.size(); ++v) {
     Rank& r = L.ranks[v];
-    launch_combine_bwd(T, H, K, dy + (L.virt ? static_cast<long long>(v) * TH : 0), r.topk_w, r.topk_idx, r.slot_dst,
-                       L.peers, r.dl, r.dl_dense, r.rw_rows, r.rw_off, st);
+    launch_combine_bwd(T, H, K, dy + (L.virt ? static_cast<long long>(v) * TH : 0), r.topk_w, r.topk_idx, r.tok_rows,
+                       r.slot_dst, L.peers, r.dl, r.dl_dense, r.rw_rows, r.rw_off, st);
     launch_router_wgrad(r.x_in, T, H, E, r.dl_dense, L.T_max, r.rw_rows, r.rw_off, r.dwg_partial, r.dwg, L.num_sms,
                         st);
   }
@@ -555,8 +562,11 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
     GroupedGemmArgs g2 = gemm_args(L, r);  // dX rows
     g2.N = H;
     g2.K = 2 * F;
-    g2.out = r.dx_rows;
+    g2.out = nullptr;  // dX rows go straight to the token owners' tok_rows (y is dead by now)
     g2.ldo = H;
+    g2.row_src = r.row_src;
+    g2.scatter = L.d_tok_table;
+    g2.scatter_rows = static_cast<long long>(L.T_max) * K;
     gemm(L, GemmKind::kBwdUpDgrad, r.tm_dh_k, r.tm_w13_mn, r.tm_w13_mn, g2, st);
   }
   CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][3], st));
@@ -570,8 +580,8 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   mark(L, st, kPhBwdGemmBarrier);
   for (size_t v = 0; v < L.ranks.size(); ++v) {
     Rank& r = L.ranks[v];
-    launch_unpermute_bwd(T, H, K, r.topk_idx, r.dl, r.slot_dst, r.wg, L.peers,
-                         dx + (L.virt ? static_cast<long long>(v) * TH : 0), st);
+    launch_unpermute_bwd(T, H, K, r.topk_idx, r.dl, r.tok_rows, r.wg, dx + (L.virt ? static_cast<long long>(v) * TH : 0),
+                         st);
   }
   mark(L, st, kPhUnpermute);
   if (N > 1 && !ce_rs)
@@ -637,6 +647,7 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     const long long worst = static_cast<long long>(d.max_tokens) * d.top_k * L->N + 128LL * L->C;
     L->cap = d.max_recv_rows ? static_cast<long long>(d.max_recv_rows) + 128LL * L->C : worst;
     require(L->cap < (1LL << 24), "receive rows must stay below 2^24");
+    require(static_cast<long long>(d.max_tokens) * d.top_k < (1LL << kRowSrcShift), "max_tokens * top_k must stay below 2^26");
     const int local = L->virt ? L->N : 1;
     L->ranks.resize(local);
     for (int v = 0; v < local; ++v) {
@@ -678,10 +689,12 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
       CK(cudaMalloc(&L->rs_stage, static_cast<size_t>(L->E) * L->N * static_cast<size_t>(L->S) * sizeof(float)));
     }
     CK(cudaMalloc(&L->d_peer_flags, sizeof(unsigned int*) * kMaxRanks));
+    CK(cudaMalloc(&L->d_tok_table, sizeof(__nv_bfloat16*) * kMaxRanks));
     if (L->virt) {
       unsigned int* f[kMaxRanks] = {};
       for (int v = 0; v < local; ++v) f[v] = L->ranks[v].flags;
       CK(cudaMemcpy(L->d_peer_flags, f, sizeof(f), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(L->d_tok_table, L->peers.tok_rows, sizeof(L->peers.tok_rows), cudaMemcpyHostToDevice));
     }
     CK(cudaDeviceSynchronize());
     *out = L.release();
@@ -699,6 +712,7 @@ void mp_fsep_layer_free(mp_fsep_layer* L) {
     cudaFree(r.priv);
   }
   cudaFree(L->d_peer_flags);
+  cudaFree(L->d_tok_table);
   cudaFreeHost(L->layout_host);
   cudaFreeHost(L->R_host);
   cudaStreamDestroy(L->side);
@@ -764,15 +778,16 @@ mp_status mp_fsep_layer_connect(mp_fsep_layer* L, const void* all_handles, const
       // identical carving on every rank -> identical offsets
       auto off = [&](const void* q) { return static_cast<const char*>(q) - static_cast<char*>(me.arena); };
       L->peers.x_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.x_rows));
-      L->peers.y_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.y_rows));
       L->peers.dy_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.dy_rows));
-      L->peers.dx_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.dx_rows));
+      L->peers.tok_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.tok_rows));
+      L->peers.row_src[p] = reinterpret_cast<int*>(base + off(me.row_src));
       L->peers.R_all[p] = reinterpret_cast<unsigned long long*>(base + off(me.R_all));
       L->peers.grad_full[p] = reinterpret_cast<float*>(base + off(me.grad_full));
       L->peers.shard[p] = reinterpret_cast<const __nv_bfloat16*>(base + off(me.shard));
       flags[p] = reinterpret_cast<unsigned int*>(base + off(me.flags));
     }
     CK(cudaMemcpy(L->d_peer_flags, flags, sizeof(flags), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(L->d_tok_table, L->peers.tok_rows, sizeof(L->peers.tok_rows), cudaMemcpyHostToDevice));
     L->connected = true;
   });
 }
@@ -917,9 +932,9 @@ mp_status mp_fsep_layer_read(mp_fsep_layer* L, const char* name, uint32_t vrank,
     else if (n == "status") src = &r.pt->status, sz = 4;
     else if (n == "total_rows") src = &r.pt->total_rows, sz = 4;
     else if (n == "x_rows") src = r.x_rows, sz = cap * H * 2;
-    else if (n == "y_rows") src = r.y_rows, sz = cap * H * 2;
     else if (n == "dy_rows") src = r.dy_rows, sz = cap * H * 2;
-    else if (n == "dx_rows") src = r.dx_rows, sz = cap * H * 2;
+    else if (n == "tok_rows") src = r.tok_rows, sz = T * K * H * 2;
+    else if (n == "row_src") src = r.row_src, sz = cap * 4;
     else if (n == "h") src = r.h, sz = cap * 2 * F * 2;
     else if (n == "act") src = r.act, sz = cap * F * 2;
     else if (n == "restored") src = r.restored, sz = C * static_cast<size_t>(L->flat) * 2;

@@ -76,6 +76,21 @@ def check_routing(layer, ref, N, T, K, C):
         assert np.array_equal(layer.read("seg_off", v).view(np.int32), rt.seg_off[v])
         assert np.array_equal(layer.read("slot_expert", v).view(np.int32), rt.slot_expert[v])
         assert layer.read("status", v).view(np.int32)[0] == 0
+    # every receive row knows its origin slot (drives the GEMM epilogue's return scatter);
+    # padding rows are marked -1
+    for d in range(N):
+        src = layer.read("row_src", d).view(np.int32)
+        seg_rows = rt.seg_rows[d]
+        seg_off = rt.seg_off[d]
+        for c in range(len(seg_rows)):
+            pad_end = seg_off[c] + (seg_rows[c] + 127) // 128 * 128
+            assert (src[seg_off[c] + seg_rows[c]:pad_end] == -1).all(), f"pad rows of slot {c} on rank {d}"
+    for v in range(N):
+        want = (v << 26) | np.arange(T * K, dtype=np.int64).reshape(T, K)
+        for d in range(N):
+            src = layer.read("row_src", d).view(np.int32)
+            m = rt.slot_dev[v] == d
+            assert np.array_equal(src[rt.slot_row[v][m]], want[m]), f"row origins of rank {v} on rank {d}"
     assert np.array_equal(layer.histogram(), rt.R)
 
 
