@@ -343,6 +343,17 @@ def main():
     sts = [layer.stats() for layer in layers]
     phases = layers[0].phase_ms() if os.environ.get("FSEP_PHASE_TIMING") == "1" else None
     comm = token_kernel_bandwidth(phases, layers[0], PL, N, rank, T, K, H) if phases else None
+    per_rank = None
+    if world > 1 and phases:
+        # per-rank view of the phases that expose load imbalance (barrier waits absorb it)
+        allp = [None] * world
+        rows = int(layers[0].read("total_rows").view(np.int32)[0])
+        dist.all_gather_object(allp, {"phases": phases, "gemm_ms": sum(s_["gemm_ms"] for s_ in sts), "rows": rows})
+        keys = ["router_scan", "dispatch", "fwd_gemms", "fwd_barrier", "combine_bwd_router_wgrad", "bwd_gemms",
+                "rs_sum_barrier", "step_total"]
+        per_rank = {k: [round(a["phases"].get(k, 0.0), 3) for a in allp] for k in keys}
+        per_rank["gemm_ms"] = [round(a["gemm_ms"], 3) for a in allp]
+        per_rank["recv_rows_last_step"] = [a["rows"] for a in allp]
     st = {"gemm_ms": sum(s_["gemm_ms"] for s_ in sts), "gemm_flops": sum(s_["gemm_flops"] for s_ in sts),
           "kernel_launches": sum(s_["kernel_launches"] for s_ in sts)}
     value = N * T / (ms * 1e-3)
@@ -456,6 +467,8 @@ def main():
             line["phases_ms_layer0"] = phases
         if comm:
             line["token_kernels_layer0"] = comm
+        if per_rank:
+            line["phases_ms_per_rank_layer0"] = per_rank
         print(json.dumps(line), flush=True)
     for layer in layers:
         layer.close()

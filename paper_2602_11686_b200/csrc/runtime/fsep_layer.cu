@@ -3,21 +3,24 @@
 //
 // Step schedule (per rank; in virtual mode every phase loops over the N
 // emulated ranks on one GPU, in real mode a peer barrier kernel separates phases):
-//   forward   layout H2D | == barrier == | shard restore (copy engines, one stream
-//             per peer, per-(slot, peer) readiness flags; virtual mode: a restore
+//   forward   layout H2D | == barrier == | shard restore: every rank PUSHES its
+//             chunk of each expert to the ranks hosting it (copy engines, one
+//             stream per destination), each copy followed by a readiness flag
+//             written into the destination's memory (virtual mode: a restore
 //             kernel on a side stream)
 //             router+top-k+histogram -> block scan (R row -> every rank's R_all)
 //             == barrier ==  plan (device lite routing) + pad zeroing
 //             R D2H + host planner callback (planner stream) -> layout of step t+1
 //             dispatch (token rows -> destination rows, peer stores)
 //             == barrier ==  GEMM gate/up + SwiGLU -> GEMM down (producer waits per
-//             slot for its restored chunks, so the restore overlaps the GEMMs)
-//             == barrier ==  combine (peer loads, gate-weighted fp32 sum)
+//             slot for its restored chunks, so the restore overlaps the GEMMs; the
+//             down GEMM's epilogue stores y rows into the token owners' slot rows)
+//             == barrier ==  combine (local slot rows, gate-weighted fp32 sum)
 //   backward  combine bwd (dw, dl; dY rows -> expert devices) + router wgrad GEMM
-//             == barrier ==  dgrad (SwiGLU'), wgrad x2 (fp32)
-//             == barrier ==  grad reduce-scatter gathers on the copy engines, under
-//             the dX GEMM that follows; owner-side sum kernel
-//             == barrier ==  unpermute bwd (+ router dx)
+//             == barrier ==  dgrad (SwiGLU'), wgrad dW2 -> push W2 grad chunks to their
+//             owners (copy engines) under the dW13 wgrad -> push W13 chunks under the
+//             dX GEMM (its epilogue stores dX rows into the owners' slot rows)
+//             == barrier ==  owner-side reduce-scatter sum, unpermute bwd (+ router dx)
 // Only the copy-engine path needs the layout on the host: the forward waits on
 // the previous step's planner callback (which ran right after that step's
 // router), so the host stays one step ahead.  Per-expert row counts never leave
@@ -75,6 +78,8 @@ struct Rank {
   float* grad_full = nullptr;
   __nv_bfloat16* shard = nullptr;
   unsigned int* flags = nullptr;
+  unsigned* ready = nullptr;   // [kMaxExperts][kMaxRanks] restore readiness (written by the pushing peers)
+  float* rs_stage = nullptr;   // [E][N][S] replica grad chunks pushed by the hosts (owner side)
   // private
   void* priv = nullptr;
   float* grad_shard = nullptr;
@@ -144,11 +149,13 @@ extern "C" struct mp_fsep_layer {
   cudaStream_t ce[kMaxRanks] = {};
   cudaEvent_t ev_ce[kMaxRanks] = {};
   cudaEvent_t ev_wg = nullptr;
-  unsigned* d_ready = nullptr;  // [kMaxExperts][kMaxRanks]
   unsigned restore_epoch = 0;
+  __nv_bfloat16* peer_restored[kMaxRanks] = {};  // every rank's restored experts (push targets)
+  unsigned* peer_ready[kMaxRanks] = {};
+  float* peer_rs_stage[kMaxRanks] = {};
+  cudaEvent_t ev_w2 = nullptr;
   uint8_t* layout_ring = nullptr;  // pinned [4][E*N] host snapshots of the layout per forward
   const uint8_t* cur_layout = nullptr;
-  float* rs_stage = nullptr;  // [E][N][S] gathered replica chunks (owner side)
   // optional per-phase event timing (FSEP_PHASE_TIMING=1)
   static constexpr int kPhaseRing = 64;
   bool phase_on = false;
@@ -248,6 +255,12 @@ void allocate_rank(Layer& L, Rank& r) {
   acc(C * flat * 4);  // grad_full
   acc(E * S * 2);    // shard
   acc((N + 1) * 4);  // flags
+  const bool push = L.ce_mode;
+  if (push) {
+    acc(C * flat * 2);                      // restored (push target)
+    acc(kMaxExperts * kMaxRanks * 4);       // ready
+    acc(E * N * S * 4);                     // rs_stage
+  }
   r.arena_bytes = align_up(a, 2 << 20);
   CK(cudaMalloc(&r.arena, r.arena_bytes));
   CK(cudaMemset(r.arena, 0, r.arena_bytes));
@@ -260,14 +273,19 @@ void allocate_rank(Layer& L, Rank& r) {
   r.grad_full = ca.take<float>(C * flat);
   r.shard = ca.take<__nv_bfloat16>(E * S);
   r.flags = ca.take<unsigned int>(N + 1);
+  if (push) {
+    r.restored = ca.take<__nv_bfloat16>(C * flat);
+    r.ready = ca.take<unsigned>(kMaxExperts * kMaxRanks);
+    r.rs_stage = ca.take<float>(E * N * S);
+  }
   // private
   const int splits = router_wgrad_splits(static_cast<int>(T));
   size_t b = 0;
   auto accp = [&](size_t bytes) { b = align_up(b, 256) + bytes; };
   const bool multi = N > 1;
   if (multi) {
-    accp(E * S * 4);       // grad_shard
-    accp(C * flat * 2);    // restored
+    accp(E * S * 4);                    // grad_shard
+    if (!push) accp(C * flat * 2);      // restored
   }
   accp(cap * 2 * F * 2);  // h
   accp(cap * F * 2);      // act
@@ -286,7 +304,7 @@ void allocate_rank(Layer& L, Rank& r) {
   Carver cp{static_cast<char*>(r.priv)};
   if (multi) {
     r.grad_shard = cp.take<float>(E * S);
-    r.restored = cp.take<__nv_bfloat16>(C * flat);
+    if (!push) r.restored = cp.take<__nv_bfloat16>(C * flat);
   } else {
     r.grad_shard = r.grad_full;  // one device: the shard IS the full expert set (C == E)
     r.restored = r.shard;
@@ -388,23 +406,27 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   barrier(L, st);
   mark(L, st, kPhParamBarrier);
   if (restore && ce) {
+    // Push: this rank's chunk of every expert goes straight into the restored
+    // slot of each rank that hosts it (own slots first), and a flag written into
+    // the destination's memory after each copy releases that (slot, source)
+    // pair to the destination's gate-up GEMM producer.
     Rank& r = L.ranks[0];
-    const std::vector<int> mine = hosted_experts(L.cur_layout, E, N, r.rank);
     ++L.restore_epoch;
     CK(cudaEventRecord(L.ev_fork, st));
     mark(L, st, kPhRestoreBegin);
     for (int q = 0; q < N; ++q) {
-      const int p = (r.rank + q) % N;  // start with the local chunk, then peers in ring order
-      CK(cudaStreamWaitEvent(L.ce[p], L.ev_fork, 0));
-      for (int c = 0; c < static_cast<int>(mine.size()); ++c) {
-        CK(cudaMemcpyAsync(r.restored + static_cast<long long>(c) * L.flat + static_cast<long long>(p) * L.S,
-                           L.peers.shard[p] + static_cast<long long>(mine[c]) * L.S, static_cast<size_t>(L.S) * 2,
-                           cudaMemcpyDeviceToDevice, L.ce[p]));
-        if (write_value_fn()(L.ce[p], reinterpret_cast<CUdeviceptr>(L.d_ready + c * N + p), L.restore_epoch, 0) !=
-            CUDA_SUCCESS)
+      const int d = (r.rank + q) % N;
+      const std::vector<int> theirs = hosted_experts(L.cur_layout, E, N, d);
+      CK(cudaStreamWaitEvent(L.ce[d], L.ev_fork, 0));
+      for (int c = 0; c < static_cast<int>(theirs.size()); ++c) {
+        CK(cudaMemcpyAsync(L.peer_restored[d] + static_cast<long long>(c) * L.flat + static_cast<long long>(r.rank) * L.S,
+                           r.shard + static_cast<long long>(theirs[c]) * L.S, static_cast<size_t>(L.S) * 2,
+                           cudaMemcpyDeviceToDevice, L.ce[d]));
+        if (write_value_fn()(L.ce[d], reinterpret_cast<CUdeviceptr>(L.peer_ready[d] + c * N + r.rank),
+                             L.restore_epoch, 0) != CUDA_SUCCESS)
           throw Error(ErrorKind::device, "cuStreamWriteValue32 failed");
       }
-      CK(cudaEventRecord(L.ev_ce[p], L.ce[p]));
+      CK(cudaEventRecord(L.ev_ce[d], L.ce[d]));
     }
   } else if (restore) {
     CK(cudaEventRecord(L.ev_fork, st));
@@ -463,7 +485,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   for (Rank& r : L.ranks) {
     GroupedGemmArgs g = gemm_args(L, r);
     if (restore && ce) {  // per-(slot, peer) readiness instead of a whole-restore join
-      g.ready = L.d_ready;
+      g.ready = r.ready;
       g.ready_epoch = L.restore_epoch;
       g.ready_n = N;
     }
@@ -516,8 +538,29 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   barrier(L, st);
   mark(L, st, kPhCombineBwdBarrier);
   CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][2], st));
-  // Weight gradients first: in copy-engine mode their reduce-scatter gathers run
-  // on the copy engines underneath the (long) dX GEMM that follows.
+  // Weight gradients first: in copy-engine mode their reduce-scatter pushes run
+  // on the copy engines underneath the GEMMs that follow (W2 part under dW13,
+  // W13 part under dX).
+  const bool ce_rs = L.ce_mode && N > 1;
+  // Push this rank's replica-gradient chunks [lo, hi) of the flat vector to their
+  // owners' staging rows (copy engines, one stream per owner), after `ev`.
+  auto push_grads = [&](cudaEvent_t ev, long long lo, long long hi) {
+    Rank& r = L.ranks[0];
+    const std::vector<int> mine = hosted_experts(L.cur_layout, E, N, r.rank);
+    for (int q = 1; q < N; ++q) {
+      const int o = (r.rank + q) % N;
+      const long long a = std::max(lo, static_cast<long long>(o) * L.S);
+      const long long b = std::min(hi, static_cast<long long>(o + 1) * L.S);
+      if (a >= b) continue;
+      CK(cudaStreamWaitEvent(L.ce[o], ev, 0));
+      for (int c = 0; c < static_cast<int>(mine.size()); ++c)
+        CK(cudaMemcpyAsync(L.peer_rs_stage[o] + (static_cast<long long>(mine[c]) * N + r.rank) * L.S + (a - o * L.S),
+                           r.grad_full + static_cast<long long>(c) * L.flat + a, static_cast<size_t>(b - a) * 4,
+                           cudaMemcpyDeviceToDevice, L.ce[o]));
+      CK(cudaEventRecord(L.ev_ce[o], L.ce[o]));
+    }
+  };
+  const long long w2_lo = 2LL * F * H;
   for (Rank& r : L.ranks) {
     GroupedGemmArgs g = gemm_args(L, r);  // dAct -> dH (SwiGLU backward fused)
     g.N = F;
@@ -534,6 +577,12 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
     g3.ldo = F;
     g3.out_group_stride = L.flat;
     gemm(L, GemmKind::kBwdWgrad, r.tm_dy_mn, r.tm_act_mn, r.tm_act_mn, g3, st);
+  }
+  if (ce_rs) {  // W2 part of the gradient chunks travels under the dW13 GEMM
+    CK(cudaEventRecord(L.ev_w2, st));
+    push_grads(L.ev_w2, w2_lo, L.flat);
+  }
+  for (Rank& r : L.ranks) {
     GroupedGemmArgs g4 = gemm_args(L, r);  // dW13 = dH^T X
     g4.M = 2 * F;
     g4.N = H;
@@ -542,21 +591,9 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
     g4.out_group_stride = L.flat;
     gemm(L, GemmKind::kBwdWgrad, r.tm_dh_mn, r.tm_x_mn, r.tm_x_mn, g4, st);
   }
-  const bool ce_rs = L.ce_mode && N > 1;
-  if (ce_rs) {
-    barrier(L, st);  // every rank's replica gradients are complete
+  if (ce_rs) {  // W13 part under the dX GEMM
     CK(cudaEventRecord(L.ev_wg, st));
-    Rank& r = L.ranks[0];
-    for (int q = 1; q < N; ++q) {
-      const int h = (r.rank + q) % N;
-      const std::vector<int> theirs = hosted_experts(L.cur_layout, E, N, h);
-      CK(cudaStreamWaitEvent(L.ce[h], L.ev_wg, 0));
-      for (int c = 0; c < static_cast<int>(theirs.size()); ++c)
-        CK(cudaMemcpyAsync(L.rs_stage + (static_cast<long long>(theirs[c]) * N + h) * L.S,
-                           L.peers.grad_full[h] + static_cast<long long>(c) * L.flat + static_cast<long long>(r.rank) * L.S,
-                           static_cast<size_t>(L.S) * 4, cudaMemcpyDeviceToDevice, L.ce[h]));
-      CK(cudaEventRecord(L.ev_ce[h], L.ce[h]));
-    }
+    push_grads(L.ev_wg, 0, w2_lo);
   }
   for (Rank& r : L.ranks) {
     GroupedGemmArgs g2 = gemm_args(L, r);  // dX rows
@@ -573,8 +610,9 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   mark(L, st, kPhBwdGemm);
   if (ce_rs) {
     Rank& r = L.ranks[0];
-    for (int q = 1; q < N; ++q) CK(cudaStreamWaitEvent(st, L.ev_ce[(r.rank + q) % N], 0));
-    launch_grad_rs_sum(r.pt, r.grad_full, L.rs_stage, E, N, r.rank, L.S, L.flat, r.grad_shard, st);
+    for (int q = 1; q < N; ++q) CK(cudaStreamWaitEvent(st, L.ev_ce[(r.rank + q) % N], 0));  // own pushes landed
+    barrier(L, st);  // ... and everyone else's
+    launch_grad_rs_sum(r.pt, r.grad_full, r.rs_stage, E, N, r.rank, L.S, L.flat, r.grad_shard, st);
   }
   barrier(L, st);
   mark(L, st, kPhBwdGemmBarrier);
@@ -648,6 +686,10 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     L->cap = d.max_recv_rows ? static_cast<long long>(d.max_recv_rows) + 128LL * L->C : worst;
     require(L->cap < (1LL << 24), "receive rows must stay below 2^24");
     require(static_cast<long long>(d.max_tokens) * d.top_k < (1LL << kRowSrcShift), "max_tokens * top_k must stay below 2^26");
+    // copy-engine communication for real multi-GPU mode (FSEP_COMM=kernel selects the SM kernels);
+    // decided before carving the arena (push targets live in it; identical on every rank)
+    const char* comm = std::getenv("FSEP_COMM");
+    L->ce_mode = !L->virt && L->N > 1 && !(comm && std::string(comm) == "kernel") && write_value_fn() != nullptr;
     const int local = L->virt ? L->N : 1;
     L->ranks.resize(local);
     for (int v = 0; v < local; ++v) {
@@ -674,19 +716,14 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
         for (auto& e : ring) CK(cudaEventCreate(&e));
     }
     if (const char* v = std::getenv("FSEP_RESTORE_BLOCKS")) L->restore_blocks = std::max(1, std::atoi(v));
-    // copy-engine communication for real multi-GPU mode (FSEP_COMM=kernel selects the SM kernels)
-    const char* comm = std::getenv("FSEP_COMM");
-    L->ce_mode = !L->virt && L->N > 1 && !(comm && std::string(comm) == "kernel") && write_value_fn() != nullptr;
     if (L->ce_mode) {
       for (int p = 0; p < L->N; ++p) {
         CK(cudaStreamCreateWithFlags(&L->ce[p], cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&L->ev_ce[p], cudaEventDisableTiming));
       }
       CK(cudaEventCreateWithFlags(&L->ev_wg, cudaEventDisableTiming));
-      CK(cudaMalloc(&L->d_ready, sizeof(unsigned) * kMaxExperts * kMaxRanks));
-      CK(cudaMemset(L->d_ready, 0, sizeof(unsigned) * kMaxExperts * kMaxRanks));
+      CK(cudaEventCreateWithFlags(&L->ev_w2, cudaEventDisableTiming));
       CK(cudaMallocHost(&L->layout_ring, 4 * static_cast<size_t>(L->E) * L->N));
-      CK(cudaMalloc(&L->rs_stage, static_cast<size_t>(L->E) * L->N * static_cast<size_t>(L->S) * sizeof(float)));
     }
     CK(cudaMalloc(&L->d_peer_flags, sizeof(unsigned int*) * kMaxRanks));
     CK(cudaMalloc(&L->d_tok_table, sizeof(__nv_bfloat16*) * kMaxRanks));
@@ -724,9 +761,8 @@ void mp_fsep_layer_free(mp_fsep_layer* L) {
       cudaEventDestroy(L->ev_ce[p]);
     }
     cudaEventDestroy(L->ev_wg);
-    cudaFree(L->d_ready);
+    cudaEventDestroy(L->ev_w2);
     cudaFreeHost(L->layout_ring);
-    cudaFree(L->rs_stage);
   }
   for (cudaEvent_t e : {L->ev_fork, L->ev_restored, L->ev_hist, L->ev_planned}) cudaEventDestroy(e);
   for (auto& ring : L->ev_g)
@@ -781,6 +817,11 @@ mp_status mp_fsep_layer_connect(mp_fsep_layer* L, const void* all_handles, const
       L->peers.dy_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.dy_rows));
       L->peers.tok_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.tok_rows));
       L->peers.row_src[p] = reinterpret_cast<int*>(base + off(me.row_src));
+      if (L->ce_mode) {
+        L->peer_restored[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.restored));
+        L->peer_ready[p] = reinterpret_cast<unsigned*>(base + off(me.ready));
+        L->peer_rs_stage[p] = reinterpret_cast<float*>(base + off(me.rs_stage));
+      }
       L->peers.R_all[p] = reinterpret_cast<unsigned long long*>(base + off(me.R_all));
       L->peers.grad_full[p] = reinterpret_cast<float*>(base + off(me.grad_full));
       L->peers.shard[p] = reinterpret_cast<const __nv_bfloat16*>(base + off(me.shard));
