@@ -7,12 +7,15 @@
 //    replica split reproduces lite_routing (planner.cpp:277-282);
 //  * every token-slot's destination (device, row) and the per-device segment
 //    layout are integer functions of R, the layout and the ranks.
+#include <cstdlib>
+#include <string>
 #include <cuda_bf16.h>
 
 #include <cfloat>
 #include <stdexcept>
 
 #include "kernels/fsep_types.cuh"
+#include "kernels/sm100_ptx.cuh"
 #include "kernels/kernels.hpp"
 #include "kernels/routing.hpp"
 
@@ -178,6 +181,85 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
 #pragma unroll
     for (int c = 0; c < CH; ++c) dst_row[k][c * 32 + lane] = v[c];
   }
+}
+
+// TMA-engine dispatch: per warp a ring of kDispatchBufs row buffers in shared
+// memory; lane 0 bulk-loads token rows (local HBM) ahead and bulk-stores each
+// row to its K destination rows (local HBM or peers over NVLink), so the
+// copies run on the TMA engine with many rows in flight per SM instead of
+// through per-thread 16-B stores.
+constexpr int kDispatchWarps = 4;
+template <int CH>
+constexpr int dispatch_bufs() { return CH >= 16 ? 3 : (CH >= 8 ? 6 : 8); }
+template <int CH>
+constexpr size_t dispatch_smem() {
+  return static_cast<size_t>(kDispatchWarps) * dispatch_bufs<CH>() * (CH * 512 + 16);
+}
+
+template <int CH>
+__global__ void __launch_bounds__(kDispatchWarps * 32) dispatch_tma_kernel(
+    const __nv_bfloat16* __restrict__ x, int T, int K, int E, const int* __restrict__ topk_idx,
+    const int* __restrict__ intra_rank, const int* __restrict__ blk_base, const PlanTables* __restrict__ pt,
+    PeerTable peers, uint32_t* __restrict__ slot_dst, int src_rank) {
+  using namespace ptx;
+  constexpr int H = CH * 256;
+  constexpr uint32_t RB = H * 2;
+  constexpr int NB = dispatch_bufs<CH>();
+  extern __shared__ __align__(128) uint8_t dsm[];
+  const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
+  uint8_t* buf = dsm + static_cast<size_t>(warp) * NB * RB;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(dsm + static_cast<size_t>(kDispatchWarps) * NB * RB) + warp * NB;
+  const int gw = blockIdx.x * kDispatchWarps + warp, nw = gridDim.x * kDispatchWarps;
+  if (lane == 0) {
+    for (int b = 0; b < NB; ++b) mbar_init(&bar[b], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto issue = [&](int j) {  // bulk-load token gw + j*nw into buffer j % NB
+    const int t = gw + j * nw;
+    if (t >= T) return;
+    uint64_t* b = &bar[j % NB];
+    mbar_arrive_expect_tx(b, RB);
+    bulk_g2s(buf + static_cast<size_t>(j % NB) * RB, x + static_cast<size_t>(t) * H, RB, b);
+  };
+  if (lane == 0)
+    for (int j = 0; j < NB; ++j) issue(j);
+  for (int j = 0;; ++j) {
+    const int t = gw + j * nw;
+    if (t >= T) break;
+    // lane k resolves slot k's destination (same rule as dispatch_kernel)
+    unsigned long long dst = 0;
+    if (lane < K) {
+      const int k = lane;
+      const int e = topk_idx[static_cast<size_t>(t) * K + k];
+      const long long r = blk_base[static_cast<size_t>(t / kBlockTokens) * E + e] + intra_rank[static_cast<size_t>(t) * K + k];
+      int h = 0;
+      while (pt->src_cum[e][h + 1] <= r) ++h;
+      const int d = pt->host_dev[e][h];
+      const long long row = pt->src_row_base[e][h] + (r - pt->src_cum[e][h]);
+      slot_dst[static_cast<size_t>(t) * K + k] = (static_cast<uint32_t>(d) << 24) | static_cast<uint32_t>(row);
+      if (static_cast<uint64_t>(row) < peers.row_capacity) {
+        peers.row_src[d][row] = (src_rank << kRowSrcShift) | (t * K + k);
+        dst = reinterpret_cast<unsigned long long>(peers.x_rows[d] + static_cast<size_t>(row) * H);
+      }
+    }
+    unsigned long long dk[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dk[k] = __shfl_sync(0xffffffffu, dst, k);
+    if (lane == 0) {
+      mbar_wait(&bar[j % NB], (j / NB) & 1);
+      const uint8_t* src = buf + static_cast<size_t>(j % NB) * RB;
+      for (int k = 0; k < K; ++k)
+        if (dk[k]) bulk_s2g(reinterpret_cast<void*>(dk[k]), src, RB);
+      bulk_commit();
+      if (j >= 1) {  // buffer of token j-1 is free once its stores have read it
+        bulk_wait_read<1>();
+        issue(j - 1 + NB);
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) bulk_wait<0>();
 }
 
 __device__ __forceinline__ const uint4* row_ptr(__nv_bfloat16* const* bufs, uint32_t code, int H) {
@@ -493,11 +575,36 @@ void launch_zero_pad(const PlanTables* pt, int C, int H, __nv_bfloat16* x_rows, 
   count_launch();
 }
 
+bool use_tma_dispatch() {
+  static const bool on = [] {
+    const char* v = std::getenv("FSEP_DISPATCH");
+    return !(v && std::string(v) == "simt");
+  }();
+  return on;
+}
+
 void launch_dispatch(const DispatchArgs& a, cudaStream_t st) {
   if (a.T == 0) return;
-  FSEP_CH_SWITCH(a.H / 256, dispatch_kernel<CH><<<(a.T + 7) / 8, 256, 0, st>>>(
-                                a.x, a.T, a.K, a.E, a.topk_idx, a.intra_rank, a.blk_base, a.pt, a.peers, a.slot_dst,
-                                a.rank));
+  if (use_tma_dispatch()) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    FSEP_CH_SWITCH(a.H / 256, {
+      constexpr size_t smem = dispatch_smem<CH>() + kDispatchWarps * dispatch_bufs<CH>() * 8;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(dispatch_tma_kernel<CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        attr = true;
+      }
+      const int blocks = std::min(sms, (a.T + kDispatchWarps - 1) / kDispatchWarps);
+      dispatch_tma_kernel<CH><<<blocks, kDispatchWarps * 32, smem, st>>>(
+          a.x, a.T, a.K, a.E, a.topk_idx, a.intra_rank, a.blk_base, a.pt, a.peers, a.slot_dst, a.rank);
+    });
+  } else {
+    FSEP_CH_SWITCH(a.H / 256, dispatch_kernel<CH><<<(a.T + 7) / 8, 256, 0, st>>>(
+                                  a.x, a.T, a.K, a.E, a.topk_idx, a.intra_rank, a.blk_base, a.pt, a.peers, a.slot_dst,
+                                  a.rank));
+  }
   count_launch();
 }
 
