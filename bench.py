@@ -226,6 +226,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-static", action="store_true")
+    ap.add_argument("--no-ep", action="store_true", help="skip the pure expert-parallel comparison (N>1)")
     ap.add_argument("--no-phases", action="store_true", help="skip per-phase device timing events")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
@@ -258,25 +259,29 @@ def main():
     cfg_json = json.dumps({"topology": {"n_nodes": 1, "devices_per_node": N, "b_intra": 9e11, "b_inter": 9e11},
                            "cost": {"v_comm": 2.0 * H, "v_comp": 6.0 * H * F, "b_comp": peaks()[0] * 1e12},
                            "model": {"n_experts": E, "capacity": C}, "planner": {"seed": SEED_PLANNER}})
-    layers = []
-    for l in range(L):
-        layer = FsepLayer(LayerSpec(E, K, H, F, T, C, world=N, rank=rank, virtual=False))
-        if N > 1:
-            layer.connect_torch_distributed()
-        # random-init weights of the named architecture (identical on every rank)
-        g = torch.Generator(device="cuda").manual_seed(SEED_DATA + 7919 * l)
-        for e in range(E):
-            w1 = (torch.randn(F, H, device="cuda", generator=g) / H ** 0.5).bfloat16()
-            w3 = (torch.randn(F, H, device="cuda", generator=g) / H ** 0.5).bfloat16()
-            w2 = (torch.randn(H, F, device="cuda", generator=g) / F ** 0.5).bfloat16()
-            layer.load_expert(e, w1, w3, w2)
-        layer.load_router((torch.randn(E, H, device="cuda", generator=g) * 0.02).bfloat16())
-        if N > 1 and args.layout == "laer":
-            layer.attach_planner(PL.Config(cfg_json), layer=l)
-        elif N > 1:
-            layer.set_layout(PL.static_ep_layout(N, E, C))
-        layers.append(layer)
-    torch.cuda.synchronize()
+    def make_layers(cap, layout, resident=False):
+        out = []
+        for l in range(L):
+            layer = FsepLayer(LayerSpec(E, K, H, F, T, cap, world=N, rank=rank, virtual=False, resident=resident))
+            if N > 1:
+                layer.connect_torch_distributed()
+            # random-init weights of the named architecture (identical on every rank)
+            g = torch.Generator(device="cuda").manual_seed(SEED_DATA + 7919 * l)
+            for e in range(E):
+                w1 = (torch.randn(F, H, device="cuda", generator=g) / H ** 0.5).bfloat16()
+                w3 = (torch.randn(F, H, device="cuda", generator=g) / H ** 0.5).bfloat16()
+                w2 = (torch.randn(H, F, device="cuda", generator=g) / F ** 0.5).bfloat16()
+                layer.load_expert(e, w1, w3, w2)
+            layer.load_router((torch.randn(E, H, device="cuda", generator=g) * 0.02).bfloat16())
+            if N > 1 and layout == "laer":
+                layer.attach_planner(PL.Config(cfg_json), layer=l)
+            elif N > 1:
+                layer.set_layout(PL.static_ep_layout(N, E, cap))
+            out.append(layer)
+        torch.cuda.synchronize()
+        return out
+
+    layers = make_layers(C, args.layout)
     # synthetic data: x ~ N(0,1), dy ~ N(0, 0.1^2), per-rank seeds; routing bias generated on the host:
     # Gumbel-top-k with Zipf(alpha) popularity, or (multi-layer config) the drifting per-iteration
     # popularity of the reference trace generator (generate_trace: Dirichlet(0.3) init, sigma 0.15 walk).
@@ -439,6 +444,21 @@ def main():
                "note": "x, dy, routing bias H2D from pinned host memory every step (double-buffered copy stream) "
                        "+ [sum y, sum dx] D2H per step, inside the timed region"}
 
+    # ---- pure expert parallelism: C = E/N, one host per expert, experts
+    # resident across steps, no restore and no gradient reduce-scatter -- same kernels
+    pure_ep = None
+    if N > 1 and args.layout == "laer" and not args.no_ep and E % N == 0:
+        for layer in layers:
+            layer.close()
+        torch.cuda.empty_cache()
+        layers = make_layers(E // N, "static", resident=True)
+        for i in range(args.warmup):
+            step(i)
+        ems_ = timed(args.steps, lambda i: step(args.warmup + i))
+        pure_ep = {"value": N * T / (ems_ * 1e-3), "ms_per_step": ems_, "capacity": E // N,
+                   "layout": "static_ep_layout(N,E,E/N), experts resident, no restore / reduce-scatter",
+                   "speedup_laer_over_ep": round(ems_ / ms, 4)}
+
     # ---- CPU baseline (rank 0 at N=1 only)
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu:
@@ -463,6 +483,8 @@ def main():
                 args.steps, "clocks": clocks}
         if static:
             line["static_ep"] = static
+        if pure_ep:
+            line["pure_ep"] = pure_ep
         if phases:
             line["phases_ms_layer0"] = phases
         if comm:

@@ -99,9 +99,18 @@ typedef struct mp_fsep_desc {
   uint32_t rank;          /* this process's rank (real mode) */
   uint32_t virtual_ranks; /* 0 = real mode (one process per GPU, N processes);
                              1 = all N ranks emulated on this GPU (tests/correctness) */
-  uint32_t flags;         /* reserved, 0 */
+  uint32_t flags;         /* MP_FSEP_FLAG_* bits, 0 = FSEP (restore + reduce-scatter every step) */
   uint64_t max_recv_rows; /* receive-buffer rows per rank; 0 = worst case T*K*N */
 } mp_fsep_desc;
+
+/* Pure expert parallelism (the baseline FSEP is compared against): every expert
+ * has exactly one host (E == N*C, fixed layout via mp_fsep_layer_set_layout, no
+ * planner), hosted experts stay restored across steps (re-restored only after
+ * set_layout / load_expert) and expert gradients stay whole on their host (no
+ * reduce-scatter); mp_fsep_layer_expert_grad then returns the gradient of
+ * experts hosted by this process's rank(s) and leaves the outputs untouched for
+ * the others. */
+#define MP_FSEP_FLAG_RESIDENT_EXPERTS 1u
 
 mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_layer** out);
 void mp_fsep_layer_free(mp_fsep_layer* layer);

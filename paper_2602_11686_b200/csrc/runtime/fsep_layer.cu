@@ -135,7 +135,8 @@ extern "C" struct mp_fsep_layer {
   long long step_no = 0, stats_from = 0;
   unsigned long long slots_sum = 0;
   int T_step = 0;
-  bool restore_every_step = true;
+  bool resident = false;       // MP_FSEP_FLAG_RESIDENT_EXPERTS: pure EP (no per-step restore / RS)
+  bool restore_dirty = true;   // resident mode: hosted experts must be (re)restored
   // graph
   cudaGraphExec_t graph = nullptr;
   const void* graph_key[5] = {};
@@ -400,7 +401,8 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   }
   // 2. shard restore on the side stream(s) (overlaps router + dispatch, and in
   //    copy-engine mode the forward GEMMs too: they wait per slot, not per step)
-  const bool restore = N > 1 && L.restore_every_step;
+  const bool restore = N > 1 && (!L.resident || L.restore_dirty);
+  if (L.resident) L.restore_dirty = false;
   mark(L, st, kPhFwdBegin);
   // peers' shards must be final (parameter load / optimizer update) before anyone gathers them
   barrier(L, st);
@@ -541,7 +543,8 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   // Weight gradients first: in copy-engine mode their reduce-scatter pushes run
   // on the copy engines underneath the GEMMs that follow (W2 part under dW13,
   // W13 part under dX).
-  const bool ce_rs = L.ce_mode && N > 1;
+  const bool rs = N > 1 && !L.resident;  // pure EP: gradients stay whole on their single host
+  const bool ce_rs = L.ce_mode && rs;
   // Push this rank's replica-gradient chunks [lo, hi) of the flat vector to their
   // owners' staging rows (copy engines, one stream per owner), after `ev`.
   auto push_grads = [&](cudaEvent_t ev, long long lo, long long hi) {
@@ -622,7 +625,7 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
                          st);
   }
   mark(L, st, kPhUnpermute);
-  if (N > 1 && !ce_rs)
+  if (rs && !ce_rs)
     for (Rank& r : L.ranks) launch_grad_reduce_scatter(r.pt, L.peers, E, r.rank, L.S, L.flat, r.grad_shard, st);
   mark(L, st, kPhGradRS);
   // join the planner stream (it finished long before the backward GEMMs did)
@@ -682,6 +685,9 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     L->flat = flat;
     L->S = flat / L->N;
     L->virt = d.virtual_ranks != 0 || L->N == 1;
+    L->resident = (d.flags & MP_FSEP_FLAG_RESIDENT_EXPERTS) != 0;
+    require(!L->resident || d.n_experts == d.world * d.capacity,
+            "resident-expert (pure EP) mode needs E == N*C (one host per expert)");
     const long long worst = static_cast<long long>(d.max_tokens) * d.top_k * L->N + 128LL * L->C;
     L->cap = d.max_recv_rows ? static_cast<long long>(d.max_recv_rows) + 128LL * L->C : worst;
     require(L->cap < (1LL << 24), "receive rows must stay below 2^24");
@@ -839,6 +845,7 @@ mp_status mp_fsep_layer_load_expert(mp_fsep_layer* L, uint32_t expert, const voi
     require(L && w1 && w3 && w2, "mp_fsep_layer_load_expert: NULL argument");
     require(expert < static_cast<uint32_t>(L->E), "expert out of range");
     CK(cudaSetDevice(L->device));
+    L->restore_dirty = true;
     auto st = static_cast<cudaStream_t>(stream);
     const size_t n1 = static_cast<size_t>(L->F) * L->H;
     __nv_bfloat16 *tmp = nullptr, *flat = nullptr;
@@ -880,14 +887,22 @@ mp_status mp_fsep_layer_set_layout(mp_fsep_layer* L, const uint8_t* A) {
       for (int d = 0; d < L->N; ++d) reps += A[e * L->N + d] ? 1 : 0;
       require(reps >= 1, "layout: every expert needs a replica");
     }
+    if (L->resident)
+      for (int e = 0; e < L->E; ++e) {
+        int reps = 0;
+        for (int d = 0; d < L->N; ++d) reps += A[e * L->N + d] ? 1 : 0;
+        require(reps == 1, "layout: resident-expert (pure EP) mode needs exactly one host per expert");
+      }
     if (L->planner_pending) CK(cudaEventSynchronize(L->ev_planned));  // don't race the planner callback
     for (int i = 0; i < L->E * L->N; ++i) L->layout_host[i] = A[i] ? 1 : 0;
+    L->restore_dirty = true;
   });
 }
 
 mp_status mp_fsep_layer_attach_planner(mp_fsep_layer* L, mp_fsep_planner* planner) {
   return guarded([&] {
     require(L, "mp_fsep_layer_attach_planner: NULL layer");
+    require(!(L->resident && planner), "resident-expert (pure EP) layers keep a fixed layout: no planner");
     if (L->planner_pending) CK(cudaEventSynchronize(L->ev_planned));
     L->planner = planner;
     L->planner_pending = false;
@@ -934,6 +949,17 @@ mp_status mp_fsep_layer_expert_grad(mp_fsep_layer* L, uint32_t expert, float* dw
     require(expert < static_cast<uint32_t>(L->E), "expert out of range");
     require(is_device_ptr(dw1) && is_device_ptr(dw3) && is_device_ptr(dw2), "grad outputs must be device pointers");
     auto st = static_cast<cudaStream_t>(stream);
+    if (L->resident && L->N > 1) {  // whole gradient on the expert's single host
+      const uint8_t* A = L->cur_layout ? L->cur_layout : L->layout_host;
+      for (Rank& r : L->ranks) {
+        const std::vector<int> mine = hosted_experts(A, L->E, L->N, r.rank);
+        const auto it = std::find(mine.begin(), mine.end(), static_cast<int>(expert));
+        if (it == mine.end()) continue;
+        launch_unpack_grad(r.grad_full + static_cast<long long>(it - mine.begin()) * L->flat, 0, L->flat, L->H, L->F,
+                           dw1, dw3, dw2, st);
+      }
+      return;
+    }
     for (Rank& r : L->ranks) {
       const long long lo = static_cast<long long>(r.rank) * L->S;
       launch_unpack_grad(r.grad_shard + static_cast<long long>(expert) * L->S, lo, lo + L->S, L->H, L->F, dw1, dw3,
@@ -1030,7 +1056,7 @@ mp_status mp_fsep_layer_phase_ms(mp_fsep_layer* L, double* out, uint32_t n) {
     const long long cnt = std::min<long long>(L->step_no - L->stats_from, mp_fsep_layer::kPhaseRing);
     require(cnt > 0, "mp_fsep_layer_phase_ms: no completed step since reset");
     std::vector<double> acc(kPhCount, 0.0);
-    const bool restore = L->N > 1 && L->restore_every_step;
+    const bool restore = L->N > 1 && !L->resident;
     for (long long s = L->step_no - cnt; s < L->step_no; ++s) {
       auto& ev = L->ev_p[static_cast<size_t>(s % mp_fsep_layer::kPhaseRing)];
       CK(cudaEventSynchronize(ev[kPhGradRS]));

@@ -39,8 +39,8 @@ def make_problem(N, E, K, H, F, T, alpha, seed):
     return dict(wg=wg, w1=w1, w3=w3, w2=w2, xs=xs, dys=dys, biases=biases)
 
 
-def run_gpu(pb, N, E, K, H, F, T, C, A, virtual=True):
-    spec = LayerSpec(E, K, H, F, T, C, world=N, virtual=virtual)
+def run_gpu(pb, N, E, K, H, F, T, C, A, virtual=True, resident=False):
+    spec = LayerSpec(E, K, H, F, T, C, world=N, virtual=virtual, resident=resident)
     layer = FsepLayer(spec)
     for e in range(E):
         layer.load_expert(e, pb["w1"][e].cuda().contiguous(), pb["w3"][e].cuda().contiguous(),
@@ -184,4 +184,25 @@ def test_planner_lag_on_device():
         history.append(R.astype(np.int64).tolist())
         spec_ = PP.SearchSpec(2, PP.mix_seed(7, 0x6C617972, 0))
         expected = np.array(PP.plan_layout(history, topo, params, C, spec_), dtype=np.uint8)
+    layer.close()
+
+
+def test_pure_ep_resident_experts():
+    """Pure-EP baseline mode (E == N*C, one host per expert, experts stay restored,
+    no gradient reduce-scatter): same numerics as FSEP; a second step reuses the
+    resident experts and must reproduce the first step exactly."""
+    N, E, K, H, F, T, C = 4, 8, 2, 256, 256, 384, 2
+    pb = make_problem(N, E, K, H, F, T, 1.2, seed=13)
+    A = PL.static_ep_layout(N, E, C)
+    ref = oracle(pb, K, A, C)
+    layer, y, dx = run_gpu(pb, N, E, K, H, F, T, C, A, resident=True)
+    check_routing(layer, ref, N, T, K, C)
+    check_numerics(layer, ref, y, dx, N, T, H, E)
+    x = torch.cat(pb["xs"]).cuda()
+    bias = torch.from_numpy(np.concatenate(pb["biases"])).cuda()
+    y2, dx2 = torch.empty_like(x), torch.empty_like(x)
+    layer.forward(x, bias, T, y2)
+    layer.backward(torch.cat(pb["dys"]).cuda(), dx2)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2) and torch.equal(dx, dx2)
     layer.close()

@@ -1,4 +1,4 @@
 N=${1:-4}
 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus $N --steps 10 --warmup 3 --no-e2e > gpurun_out/bench_n${N}.json 2> gpurun_out/bench_n${N}.err; echo mix=$?
+python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus $N --steps 10 --warmup 3 > gpurun_out/bench_n${N}.json 2> gpurun_out/bench_n${N}.err; echo mix=$?
 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus $N --config fine --steps 10 --warmup 3 --no-e2e > gpurun_out/bench_n${N}_fine.json 2> gpurun_out/bench_n${N}_fine.err; echo fine=$?
