@@ -196,6 +196,11 @@ def token_kernel_bandwidth(phases, layer, PL, N, rank, T, K, H):
         R = layer.histogram()
         A = layer.read("layout").reshape(R.shape[1], N)
         S = PL.lite_routing(R, A)[rank]  # [E, dst]
+        if getattr(layer.spec, "local_first", False):
+            for e in range(S.shape[0]):
+                if A[e, rank]:
+                    S[e, :] = 0
+                    S[e, rank] = R[rank, e]
         remote = int(S.sum() - S[:, rank].sum())
     out = {}
     for name, ph in (("dispatch", "dispatch"), ("combine", "combine"), ("unpermute", "unpermute")):
@@ -227,6 +232,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-static", action="store_true")
     ap.add_argument("--no-ep", action="store_true", help="skip the pure expert-parallel comparison (N>1)")
+    ap.add_argument("--routing", default="lite", choices=["lite", "local_first"],
+                    help="token routing: the reference lite_routing (default) or the local-first variant")
+    ap.add_argument("--no-local-first", action="store_true", help="skip the local-first routing comparison (N>1)")
     ap.add_argument("--no-phases", action="store_true", help="skip per-phase device timing events")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
@@ -259,10 +267,11 @@ def main():
     cfg_json = json.dumps({"topology": {"n_nodes": 1, "devices_per_node": N, "b_intra": 9e11, "b_inter": 9e11},
                            "cost": {"v_comm": 2.0 * H, "v_comp": 6.0 * H * F, "b_comp": peaks()[0] * 1e12},
                            "model": {"n_experts": E, "capacity": C}, "planner": {"seed": SEED_PLANNER}})
-    def make_layers(cap, layout, resident=False):
+    def make_layers(cap, layout, resident=False, local_first=False):
         out = []
         for l in range(L):
-            layer = FsepLayer(LayerSpec(E, K, H, F, T, cap, world=N, rank=rank, virtual=False, resident=resident))
+            layer = FsepLayer(LayerSpec(E, K, H, F, T, cap, world=N, rank=rank, virtual=False, resident=resident,
+                                        local_first=local_first))
             if N > 1:
                 layer.connect_torch_distributed()
             # random-init weights of the named architecture (identical on every rank)
@@ -281,7 +290,7 @@ def main():
         torch.cuda.synchronize()
         return out
 
-    layers = make_layers(C, args.layout)
+    layers = make_layers(C, args.layout, local_first=args.routing == "local_first")
     # synthetic data: x ~ N(0,1), dy ~ N(0, 0.1^2), per-rank seeds; routing bias generated on the host:
     # Gumbel-top-k with Zipf(alpha) popularity, or (multi-layer config) the drifting per-iteration
     # popularity of the reference trace generator (generate_trace: Dirichlet(0.3) init, sigma 0.15 walk).
@@ -459,6 +468,20 @@ def main():
                    "layout": "static_ep_layout(N,E,E/N), experts resident, no restore / reduce-scatter",
                    "speedup_laer_over_ep": round(ems_ / ms, 4)}
 
+    # ---- local-first token routing (NOT the reference lite_routing)
+    local_first = None
+    if N > 1 and args.layout == "laer" and args.routing == "lite" and not args.no_local_first:
+        for layer in layers:
+            layer.close()
+        torch.cuda.empty_cache()
+        layers = make_layers(C, "laer", local_first=True)
+        for i in range(args.warmup):
+            step(i)
+        lms = timed(args.steps, lambda i: step(args.warmup + i))
+        local_first = {"value": N * T / (lms * 1e-3), "ms_per_step": lms,
+                       "routing": "local-first (non-parity variant): sources hosting a replica keep their tokens",
+                       "speedup_over_lite_routing": round(ms / lms, 4)}
+
     # ---- CPU baseline (rank 0 at N=1 only)
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu:
@@ -478,6 +501,8 @@ def main():
                            "routing": ("drifting trace popularity alpha=%g sigma=%g" % tuple(cfg["drift"]))
                            if cfg.get("drift") else f"Zipf({args.alpha}) Gumbel-top-k",
                            "layout": args.layout if N > 1 else "single device (C=E)",
+                           "token_routing": "lite_routing (reference, planner.cpp:238-287)" if args.routing == "lite"
+                           else "local-first (non-parity variant)",
                            "parallelism": f"fsep{N}", "l2": "inputs larger than L2 (x 128 MiB + weights)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": st["kernel_launches"] *
                 args.steps, "clocks": clocks}
@@ -485,6 +510,8 @@ def main():
             line["static_ep"] = static
         if pure_ep:
             line["pure_ep"] = pure_ep
+        if local_first:
+            line["local_first_routing"] = local_first
         if phases:
             line["phases_ms_layer0"] = phases
         if comm:

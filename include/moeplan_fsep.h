@@ -111,6 +111,13 @@ typedef struct mp_fsep_desc {
  * experts hosted by this process's rank(s) and leaves the outputs untouched for
  * the others. */
 #define MP_FSEP_FLAG_RESIDENT_EXPERTS 1u
+/* Local-first token routing (NOT the reference's lite_routing, planner.cpp:238-287;
+ * opt-in, labelled non-parity): a source rank that hosts a replica of expert e
+ * keeps all of its e-tokens local; other sources split their e-tokens over e's
+ * replicas by lite routing's share/remainder rule.  Cuts NVLink token traffic on
+ * one NVSwitch node; replica loads stay near-balanced when ranks see similar
+ * routing distributions. */
+#define MP_FSEP_FLAG_LOCAL_FIRST 2u
 
 mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_layer** out);
 void mp_fsep_layer_free(mp_fsep_layer* layer);

@@ -78,9 +78,13 @@ class Routing:
     slot_expert: np.ndarray      # [N, C]
 
 
-def route(idx_list, w_list, A: np.ndarray, E: int, C: int) -> Routing:
+def route(idx_list, w_list, A: np.ndarray, E: int, C: int, local_first: bool = False) -> Routing:
     """Token-slot destinations under layout A (E x N), following lite routing's
-    share/remainder split (planner.cpp:277-282) with slots ranked by token order."""
+    share/remainder split (planner.cpp:277-282) with slots ranked by token order.
+
+    local_first (NOT the reference algorithm; the runtime's opt-in
+    MP_FSEP_FLAG_LOCAL_FIRST variant): a source that hosts a
+    replica of e keeps all its e-tokens local; other sources split as above."""
     N = len(idx_list)
     R = np.zeros((N, E), dtype=np.uint64)
     for i, idx in enumerate(idx_list):
@@ -90,6 +94,12 @@ def route(idx_list, w_list, A: np.ndarray, E: int, C: int) -> Routing:
     S = np.zeros((N, E, N), dtype=np.uint64)
     for (s, e, d, tok) in P.lite_routing(R.tolist(), Al, topo):
         S[s, e, d] = tok
+    if local_first:
+        for s_ in range(N):
+            for e in range(E):
+                if A[e, s_]:
+                    S[s_, e, :] = 0
+                    S[s_, e, s_] = R[s_, e]
     hosts = [[d for d in range(N) if A[e, d]] for e in range(E)]
     slot_expert = np.zeros((N, C), dtype=np.int64)
     seg_rows = np.zeros((N, C), dtype=np.int64)
@@ -132,7 +142,8 @@ def _silu(g):
     return g / (1.0 + np.exp(-g))
 
 
-def layer_step(xs, biases, wg, w1, w3, w2, K: int, A: np.ndarray, C: int, dys, dtype=np.float64):
+def layer_step(xs, biases, wg, w1, w3, w2, K: int, A: np.ndarray, C: int, dys, dtype=np.float64,
+               local_first: bool = False):
     """Forward + backward of the FSEP layer over N ranks.
 
     xs/dys: per-rank [T, H] (bf16 values as float32); wg [E, H]; w1/w3 [E, F, H];
@@ -148,7 +159,7 @@ def layer_step(xs, biases, wg, w1, w3, w2, K: int, A: np.ndarray, C: int, dys, d
         idx_l.append(idx)
         w_l.append(w)
         logit_l.append(lg)
-    rt = route(idx_l, w_l, A, E, C) if A is not None else None
+    rt = route(idx_l, w_l, A, E, C, local_first) if A is not None else None
     f64 = dtype  # float64 for parity checks; float32 (BLAS sgemm) for the timed CPU baseline
     ys, dxs = [], []
     dW1 = np.zeros(w1.shape, dtype=f64)

@@ -67,8 +67,19 @@ __device__ __forceinline__ long long split_amount(long long tokens, int n, int t
 
 // Lite routing on device (planner.cpp:238-287 for a single-node topology) and
 // the receive layout of every device.  One block; E <= 128, N <= 16.
+// Tokens source i sends to host index t of expert e: lite routing's even split
+// (planner.cpp:277-282), or -- local-first variant -- everything to itself when
+// i hosts a replica of e.
+__device__ __forceinline__ long long route_amount(const unsigned long long* R_all, const uint8_t* layout,
+                                                  const PlanTables* pt, int E, int N, int i, int e, int t, int nh,
+                                                  bool local_first) {
+  const long long tokens = static_cast<long long>(R_all[i * E + e]);
+  if (local_first && layout[e * N + i]) return pt->host_dev[e][t] == i ? tokens : 0;
+  return split_amount(tokens, nh, t);
+}
+
 __global__ void plan_kernel(const unsigned long long* __restrict__ R_all, const uint8_t* __restrict__ layout, int E,
-                            int N, int rank, PlanTables* __restrict__ pt, long long row_capacity) {
+                            int N, int rank, PlanTables* __restrict__ pt, long long row_capacity, bool local_first) {
   __shared__ int s_seg_off[kMaxRanks][kMaxExperts];
   const int tid = threadIdx.x;
   for (int e = tid; e < E; e += blockDim.x) {
@@ -91,7 +102,7 @@ __global__ void plan_kernel(const unsigned long long* __restrict__ R_all, const 
       int t = 0;
       while (pt->host_dev[e][t] != d) ++t;
       long long rows = 0;
-      for (int i = 0; i < N; ++i) rows += split_amount(static_cast<long long>(R_all[i * E + e]), nh, t);
+      for (int i = 0; i < N; ++i) rows += route_amount(R_all, layout, pt, E, N, i, e, t, nh, local_first);
       pt->slot_of[e][d] = c;
       s_seg_off[d][c] = static_cast<int>(off);
       if (d == rank) {
@@ -112,15 +123,14 @@ __global__ void plan_kernel(const unsigned long long* __restrict__ R_all, const 
   // this rank as a source: per expert, cumulative split and destination rows
   for (int e = tid; e < E; e += blockDim.x) {
     const int nh = pt->n_hosts[e];
-    const long long tokens = static_cast<long long>(R_all[rank * E + e]);
     long long cum = 0;
     for (int t = 0; t < nh; ++t) {
       const int d = pt->host_dev[e][t];
       long long before = 0;  // rows from lower-ranked sources on d for e
-      for (int i = 0; i < rank; ++i) before += split_amount(static_cast<long long>(R_all[i * E + e]), nh, t);
+      for (int i = 0; i < rank; ++i) before += route_amount(R_all, layout, pt, E, N, i, e, t, nh, local_first);
       pt->src_cum[e][t] = cum;
       pt->src_row_base[e][t] = s_seg_off[d][pt->slot_of[e][d]] + before;
-      cum += split_amount(tokens, nh, t);
+      cum += route_amount(R_all, layout, pt, E, N, rank, e, t, nh, local_first);
     }
     pt->src_cum[e][nh] = cum;
   }
@@ -564,8 +574,8 @@ void launch_block_scan(const int* blk_hist, int nblk, int E, int* blk_base, cons
 }
 
 void launch_plan(const unsigned long long* R_all, const uint8_t* layout, int E, int N, int rank, PlanTables* pt,
-                 long long row_capacity, cudaStream_t st) {
-  plan_kernel<<<1, 128, 0, st>>>(R_all, layout, E, N, rank, pt, row_capacity);
+                 long long row_capacity, bool local_first, cudaStream_t st) {
+  plan_kernel<<<1, 128, 0, st>>>(R_all, layout, E, N, rank, pt, row_capacity, local_first);
   count_launch();
 }
 

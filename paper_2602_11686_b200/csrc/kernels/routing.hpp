@@ -36,7 +36,7 @@ void launch_router(const RouterArgs& a, cudaStream_t st);
 void launch_block_scan(const int* blk_hist, int nblk, int E, int* blk_base, const PeerTable& peers, int rank,
                        int world, cudaStream_t st);
 void launch_plan(const unsigned long long* R_all, const uint8_t* layout, int E, int N, int rank, PlanTables* pt,
-                 long long row_capacity, cudaStream_t st);
+                 long long row_capacity, bool local_first, cudaStream_t st);
 void launch_zero_pad(const PlanTables* pt, int C, int H, __nv_bfloat16* x_rows, __nv_bfloat16* dy_rows,
                      int* row_src, cudaStream_t st);
 void launch_dispatch(const DispatchArgs& a, cudaStream_t st);

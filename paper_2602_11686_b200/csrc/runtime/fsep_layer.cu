@@ -137,6 +137,7 @@ extern "C" struct mp_fsep_layer {
   int T_step = 0;
   bool resident = false;       // MP_FSEP_FLAG_RESIDENT_EXPERTS: pure EP (no per-step restore / RS)
   bool restore_dirty = true;   // resident mode: hosted experts must be (re)restored
+  bool local_first = false;    // MP_FSEP_FLAG_LOCAL_FIRST (non-parity routing variant)
   // graph
   cudaGraphExec_t graph = nullptr;
   const void* graph_key[5] = {};
@@ -453,7 +454,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   mark(L, st, kPhRBarrier);
   // 4. device lite routing + receive layout; dispatch
   for (Rank& r : L.ranks) {
-    launch_plan(r.R_all, r.layout_dev, E, N, r.rank, r.pt, L.cap, st);
+    launch_plan(r.R_all, r.layout_dev, E, N, r.rank, r.pt, L.cap, L.local_first, st);
     launch_zero_pad(r.pt, C, H, r.x_rows, r.dy_rows, r.row_src, st);
   }
   mark(L, st, kPhPlan);
@@ -686,6 +687,7 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     L->S = flat / L->N;
     L->virt = d.virtual_ranks != 0 || L->N == 1;
     L->resident = (d.flags & MP_FSEP_FLAG_RESIDENT_EXPERTS) != 0;
+    L->local_first = (d.flags & MP_FSEP_FLAG_LOCAL_FIRST) != 0;
     require(!L->resident || d.n_experts == d.world * d.capacity,
             "resident-expert (pure EP) mode needs E == N*C (one host per expert)");
     const long long worst = static_cast<long long>(d.max_tokens) * d.top_k * L->N + 128LL * L->C;

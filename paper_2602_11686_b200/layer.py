@@ -37,6 +37,7 @@ class LayerSpec:
     virtual: bool = False
     max_recv_rows: int = 0
     resident: bool = False  # MP_FSEP_FLAG_RESIDENT_EXPERTS: pure EP baseline (E == N*C, fixed layout)
+    local_first: bool = False  # MP_FSEP_FLAG_LOCAL_FIRST: non-parity local-first token routing
 
 
 def _stream(stream=None):
@@ -59,7 +60,8 @@ class FsepLayer:
         self.spec = spec
         self.device = torch.cuda.current_device() if device is None else device
         d = FsepDesc(spec.n_experts, spec.top_k, spec.hidden, spec.ffn, spec.max_tokens, spec.capacity, spec.world,
-                     spec.rank, 1 if spec.virtual else 0, 1 if spec.resident else 0, spec.max_recv_rows)
+                     spec.rank, 1 if spec.virtual else 0,
+                     (1 if spec.resident else 0) | (2 if spec.local_first else 0), spec.max_recv_rows)
         h = C.c_void_p()
         check(self.lib.mp_fsep_layer_create(C.byref(d), self.device, C.byref(h)))
         self._h = h

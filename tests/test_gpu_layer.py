@@ -39,8 +39,8 @@ def make_problem(N, E, K, H, F, T, alpha, seed):
     return dict(wg=wg, w1=w1, w3=w3, w2=w2, xs=xs, dys=dys, biases=biases)
 
 
-def run_gpu(pb, N, E, K, H, F, T, C, A, virtual=True, resident=False):
-    spec = LayerSpec(E, K, H, F, T, C, world=N, virtual=virtual, resident=resident)
+def run_gpu(pb, N, E, K, H, F, T, C, A, virtual=True, resident=False, local_first=False):
+    spec = LayerSpec(E, K, H, F, T, C, world=N, virtual=virtual, resident=resident, local_first=local_first)
     layer = FsepLayer(spec)
     for e in range(E):
         layer.load_expert(e, pb["w1"][e].cuda().contiguous(), pb["w3"][e].cuda().contiguous(),
@@ -58,10 +58,10 @@ def run_gpu(pb, N, E, K, H, F, T, C, A, virtual=True, resident=False):
     return layer, y, dx
 
 
-def oracle(pb, K, A, C):
+def oracle(pb, K, A, C, local_first=False):
     f32 = lambda t: t.float().numpy()
     return LO.layer_step([f32(x) for x in pb["xs"]], pb["biases"], f32(pb["wg"]), f32(pb["w1"]), f32(pb["w3"]),
-                         f32(pb["w2"]), K, A, C, [f32(d) for d in pb["dys"]])
+                         f32(pb["w2"]), K, A, C, [f32(d) for d in pb["dys"]], local_first=local_first)
 
 
 def check_routing(layer, ref, N, T, K, C):
@@ -205,4 +205,23 @@ def test_pure_ep_resident_experts():
     layer.backward(torch.cat(pb["dys"]).cuda(), dx2)
     torch.cuda.synchronize()
     assert torch.equal(y, y2) and torch.equal(dx, dx2)
+    layer.close()
+
+
+def test_local_first_routing_variant():
+    """Opt-in local-first token routing (non-parity variant): sources hosting a
+    replica keep their tokens; routing bit-exact vs the oracle's variant, numerics
+    unchanged (layout-independent)."""
+    N, E, K, H, F, T, C = 4, 8, 2, 256, 256, 384, 4
+    pb = make_problem(N, E, K, H, F, T, 1.2, seed=21)
+    A = PL.plan_layout(oracle(pb, K, PL.even_replication_layout(N, E, C), C)["routing"].R, C)
+    ref = oracle(pb, K, A, C, local_first=True)
+    rt = ref["routing"]
+    for s_ in range(N):  # the variant's defining property
+        for e in range(E):
+            if A[e, s_]:
+                assert rt.S[s_, e, s_] == rt.R[s_, e]
+    layer, y, dx = run_gpu(pb, N, E, K, H, F, T, C, A, local_first=True)
+    check_routing(layer, ref, N, T, K, C)
+    check_numerics(layer, ref, y, dx, N, T, H, E)
     layer.close()
