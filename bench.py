@@ -235,6 +235,8 @@ def main():
     ap.add_argument("--routing", default="lite", choices=["lite", "local_first"],
                     help="token routing: the reference lite_routing (default) or the local-first variant")
     ap.add_argument("--no-local-first", action="store_true", help="skip the local-first routing comparison (N>1)")
+    ap.add_argument("--no-prefetch", action="store_true",
+                    help="multi-layer: do not chain layers (each layer restores at its own forward)")
     ap.add_argument("--no-phases", action="store_true", help="skip per-phase device timing events")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
@@ -287,6 +289,9 @@ def main():
             elif N > 1:
                 layer.set_layout(PL.static_ep_layout(N, E, cap))
             out.append(layer)
+        if L > 1 and N > 1 and not args.no_prefetch:  # Fig.5: layer l+1's restore under layer l's MLP
+            for l in range(L - 1):
+                out[l].chain(out[l + 1])
         torch.cuda.synchronize()
         return out
 
@@ -503,7 +508,8 @@ def main():
                            "layout": args.layout if N > 1 else "single device (C=E)",
                            "token_routing": "lite_routing (reference, planner.cpp:238-287)" if args.routing == "lite"
                            else "local-first (non-parity variant)",
-                           "parallelism": f"fsep{N}", "l2": "inputs larger than L2 (x 128 MiB + weights)"},
+                           "parallelism": f"fsep{N}",
+                           "cross_layer_prefetch": L > 1 and N > 1 and not args.no_prefetch, "l2": "inputs larger than L2 (x 128 MiB + weights)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": st["kernel_launches"] *
                 args.steps, "clocks": clocks}
         if static:

@@ -152,6 +152,13 @@ mp_status mp_fsep_layer_set_layout(mp_fsep_layer* layer, const uint8_t* A);
  * layer or be detached first. */
 mp_status mp_fsep_layer_attach_planner(mp_fsep_layer* layer, mp_fsep_planner* planner);
 
+/* Layer chaining (PAPER Fig.5 schedule): after `layer`'s dispatch in each forward,
+ * the shard restore of `next` (the next MoE layer, same devices) is issued on
+ * next's copy engines, so it overlaps `layer`'s expert MLP; next's forward then
+ * skips its own restore.  Copy-engine mode (real multi-GPU) only; NULL unchains.
+ * Both layers' forwards must run every step in order (layer, then next). */
+mp_status mp_fsep_layer_chain(mp_fsep_layer* layer, mp_fsep_layer* next);
+
 /* Forward / backward of one step.  n_tokens <= max_tokens (per rank). */
 mp_status mp_fsep_layer_forward(mp_fsep_layer* layer, const void* x, const float* bias, uint32_t n_tokens,
                                 void* y, void* stream);

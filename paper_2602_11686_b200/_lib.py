@@ -87,6 +87,7 @@ _SIGS = {
     "mp_fsep_layer_load_router": (C.c_int, [vp, vp, vp]),
     "mp_fsep_layer_set_layout": (C.c_int, [vp, u8p]),
     "mp_fsep_layer_attach_planner": (C.c_int, [vp, vp]),
+    "mp_fsep_layer_chain": (C.c_int, [vp, vp]),
     "mp_fsep_layer_forward": (C.c_int, [vp, vp, vp, u32, vp, vp]),
     "mp_fsep_layer_backward": (C.c_int, [vp, vp, vp, vp]),
     "mp_fsep_layer_histogram": (C.c_int, [vp, u64p]),

@@ -138,6 +138,8 @@ extern "C" struct mp_fsep_layer {
   bool resident = false;       // MP_FSEP_FLAG_RESIDENT_EXPERTS: pure EP (no per-step restore / RS)
   bool restore_dirty = true;   // resident mode: hosted experts must be (re)restored
   bool local_first = false;    // MP_FSEP_FLAG_LOCAL_FIRST (non-parity routing variant)
+  mp_fsep_layer* next = nullptr;  // chained next layer: its restore is issued after this layer's dispatch
+  bool prefetched = false;        // this layer's restore for the coming forward is already in flight
   // graph
   cudaGraphExec_t graph = nullptr;
   const void* graph_key[5] = {};
@@ -379,6 +381,43 @@ GroupedGemmArgs gemm_args(Layer& L, Rank& r) {
   return g;
 }
 
+// Copy-engine mode: snapshot this step's layout on the host (waiting for the
+// previous step's planner callback) and ship it to the device on `st`.
+void snapshot_layout(Layer& L, cudaStream_t st) {
+  const int E = L.E, N = L.N;
+  if (L.planner_pending) CK(cudaEventSynchronize(L.ev_planned));
+  uint8_t* snap = L.layout_ring + (L.step_no % 4) * static_cast<size_t>(E) * N;
+  std::memcpy(snap, L.layout_host, static_cast<size_t>(E) * N);
+  L.cur_layout = snap;
+  for (Rank& r : L.ranks) CK(cudaMemcpyAsync(r.layout_dev, snap, static_cast<size_t>(E) * N, cudaMemcpyHostToDevice, st));
+}
+
+// Push restore: this rank's chunk of every expert goes straight into the
+// restored slot of each rank that hosts it (own slots first), and a flag written
+// into the destination's memory after each copy releases that (slot, source)
+// pair to the destination's gate-up GEMM producer.  Ordered after `st`'s work.
+void push_restore(Layer& L, cudaStream_t st) {
+  const int E = L.E, N = L.N;
+  Rank& r = L.ranks[0];
+  ++L.restore_epoch;
+  CK(cudaEventRecord(L.ev_fork, st));
+  mark(L, st, kPhRestoreBegin);
+  for (int q = 0; q < N; ++q) {
+    const int d = (r.rank + q) % N;
+    const std::vector<int> theirs = hosted_experts(L.cur_layout, E, N, d);
+    CK(cudaStreamWaitEvent(L.ce[d], L.ev_fork, 0));
+    for (int c = 0; c < static_cast<int>(theirs.size()); ++c) {
+      CK(cudaMemcpyAsync(L.peer_restored[d] + static_cast<long long>(c) * L.flat + static_cast<long long>(r.rank) * L.S,
+                         r.shard + static_cast<long long>(theirs[c]) * L.S, static_cast<size_t>(L.S) * 2,
+                         cudaMemcpyDeviceToDevice, L.ce[d]));
+      if (write_value_fn()(L.ce[d], reinterpret_cast<CUdeviceptr>(L.peer_ready[d] + c * N + r.rank), L.restore_epoch,
+                           0) != CUDA_SUCCESS)
+        throw Error(ErrorKind::device, "cuStreamWriteValue32 failed");
+    }
+    CK(cudaEventRecord(L.ev_ce[d], L.ce[d]));
+  }
+}
+
 void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __nv_bfloat16* y, cudaStream_t st) {
   if (T < 0 || T > L.T_max) throw Error(ErrorKind::invalid_argument, "forward: n_tokens exceeds max_tokens");
   const int E = L.E, K = L.K, H = L.H, F = L.F, N = L.N, C = L.C;
@@ -386,15 +425,13 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   const long long TH = static_cast<long long>(T) * H;
   // 1. layout for this step (planner result of the previous step, or set_layout)
   const bool ce = L.ce_mode;
+  const bool prefetched = L.prefetched;  // chained: layout + restore already issued by the previous layer
+  L.prefetched = false;
   if (ce) {
     // Copy-engine restore needs the layout on the host: wait for the previous
     // step's planner callback (it ran right after that step's router, so the
     // host stays up to one step ahead) and snapshot it for this step.
-    if (L.planner_pending) CK(cudaEventSynchronize(L.ev_planned));
-    uint8_t* snap = L.layout_ring + (L.step_no % 4) * static_cast<size_t>(E) * N;
-    std::memcpy(snap, L.layout_host, static_cast<size_t>(E) * N);
-    L.cur_layout = snap;
-    for (Rank& r : L.ranks) CK(cudaMemcpyAsync(r.layout_dev, snap, static_cast<size_t>(E) * N, cudaMemcpyHostToDevice, st));
+    if (!prefetched) snapshot_layout(L, st);
   } else {
     if (L.planner_pending) CK(cudaStreamWaitEvent(st, L.ev_planned, 0));
     for (Rank& r : L.ranks)
@@ -409,28 +446,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   barrier(L, st);
   mark(L, st, kPhParamBarrier);
   if (restore && ce) {
-    // Push: this rank's chunk of every expert goes straight into the restored
-    // slot of each rank that hosts it (own slots first), and a flag written into
-    // the destination's memory after each copy releases that (slot, source)
-    // pair to the destination's gate-up GEMM producer.
-    Rank& r = L.ranks[0];
-    ++L.restore_epoch;
-    CK(cudaEventRecord(L.ev_fork, st));
-    mark(L, st, kPhRestoreBegin);
-    for (int q = 0; q < N; ++q) {
-      const int d = (r.rank + q) % N;
-      const std::vector<int> theirs = hosted_experts(L.cur_layout, E, N, d);
-      CK(cudaStreamWaitEvent(L.ce[d], L.ev_fork, 0));
-      for (int c = 0; c < static_cast<int>(theirs.size()); ++c) {
-        CK(cudaMemcpyAsync(L.peer_restored[d] + static_cast<long long>(c) * L.flat + static_cast<long long>(r.rank) * L.S,
-                           r.shard + static_cast<long long>(theirs[c]) * L.S, static_cast<size_t>(L.S) * 2,
-                           cudaMemcpyDeviceToDevice, L.ce[d]));
-        if (write_value_fn()(L.ce[d], reinterpret_cast<CUdeviceptr>(L.peer_ready[d] + c * N + r.rank),
-                             L.restore_epoch, 0) != CUDA_SUCCESS)
-          throw Error(ErrorKind::device, "cuStreamWriteValue32 failed");
-      }
-      CK(cudaEventRecord(L.ev_ce[d], L.ce[d]));
-    }
+    if (!prefetched) push_restore(L, st);
   } else if (restore) {
     CK(cudaEventRecord(L.ev_fork, st));
     CK(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
@@ -479,6 +495,15 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
                                  r.rank},
                     st);
   mark(L, st, kPhDispatch);
+  // Fig.5 schedule: the next layer's expert restore travels on the copy engines
+  // while this layer's expert MLP runs (safe: every rank has passed this step's
+  // parameter barrier, so all of the previous step's work is complete).
+  if (L.next && L.next->ce_mode && !L.next->prefetched && (!L.next->resident || L.next->restore_dirty)) {
+    Layer& nx = *L.next;
+    snapshot_layout(nx, st);
+    push_restore(nx, st);
+    nx.prefetched = true;
+  }
   barrier(L, st);
   mark(L, st, kPhDispatchBarrier);
   // 5. expert FFN on the restored experts
@@ -898,6 +923,15 @@ mp_status mp_fsep_layer_set_layout(mp_fsep_layer* L, const uint8_t* A) {
     if (L->planner_pending) CK(cudaEventSynchronize(L->ev_planned));  // don't race the planner callback
     for (int i = 0; i < L->E * L->N; ++i) L->layout_host[i] = A[i] ? 1 : 0;
     L->restore_dirty = true;
+  });
+}
+
+mp_status mp_fsep_layer_chain(mp_fsep_layer* L, mp_fsep_layer* next) {
+  return guarded([&] {
+    require(L, "mp_fsep_layer_chain: NULL layer");
+    require(next != L, "mp_fsep_layer_chain: a layer cannot precede itself");
+    require(!next || (next->N == L->N && next->device == L->device), "mp_fsep_layer_chain: layers must share devices");
+    L->next = next;
   });
 }
 

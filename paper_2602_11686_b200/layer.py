@@ -107,6 +107,10 @@ class FsepLayer:
         check(self.lib.mp_fsep_layer_attach_planner(self._h, self._planner._h))
         return self._planner
 
+    def chain(self, next_layer: Optional["FsepLayer"]) -> None:
+        """Issue next_layer's shard restore after this layer's dispatch (PAPER Fig.5)."""
+        check(self.lib.mp_fsep_layer_chain(self._h, next_layer._h if next_layer is not None else None))
+
     def detach_planner(self) -> None:
         check(self.lib.mp_fsep_layer_attach_planner(self._h, None))
         self._planner = None
@@ -178,6 +182,7 @@ class FsepLayer:
         if getattr(self, "_h", None):
             if self._planner is not None:
                 self.lib.mp_fsep_layer_attach_planner(self._h, None)
+            self.lib.mp_fsep_layer_chain(self._h, None)
             self.lib.mp_fsep_layer_free(self._h)
             self._h = None
 
