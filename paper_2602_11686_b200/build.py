@@ -80,7 +80,7 @@ def build(verbose: bool = False, force: bool = False, jobs: int | None = None) -
            "-Wno-unused-function", "-isystem", str(_cuda_home() / "include")] + inc
     nvcc = [str(_cuda_home() / "bin" / "nvcc"), "-std=c++20", "-O3", "-lineinfo", *ARCH,
             "-Xcompiler", "-fPIC,-ffp-contract=off", "--expt-relaxed-constexpr",
-            "-Xptxas", "-v" if verbose else "-O3"] + inc
+            "-Xptxas", "-v" if verbose else "-O3"] + os.environ.get("FSEP_NVCC_EXTRA", "").split() + inc
     jobs_ = []
     objs = []
     for src in host + cuda:

@@ -31,7 +31,12 @@ constexpr int HALF = 128;                       // rows of A / columns of B per 
 constexpr int A_BYTES = HALF * BK * 2;          // 16 KB
 constexpr int B_BYTES = HALF * BK * 2;          // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // per CTA
-constexpr int EPI_WARPS = 8;
+#ifndef FSEP_EPI_WARPS
+#define FSEP_EPI_WARPS 8
+#endif
+constexpr int EPI_WARPS = FSEP_EPI_WARPS;  // 8: 4 TMEM lane quarters x 2 column halves; 4: quarters, both halves each
+static_assert(EPI_WARPS == 8 || EPI_WARPS == 4, "epilogue warps must be 4 or 8");
+constexpr int NHALF = EPI_WARPS == 8 ? 1 : 2;  // column halves per epilogue warp
 constexpr int THREADS = 64 + EPI_WARPS * 32;
 constexpr int MAX_GROUPS = 256;
 constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 512 + (MAX_GROUPS + 1) * 4;
@@ -248,7 +253,7 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
     const uint32_t quarter = warp & 3;
-    const int half = static_cast<int>(warp - 2) >> 2;
+    const int half0 = NHALF == 1 ? static_cast<int>(warp - 2) >> 2 : 0;
     const int r = static_cast<int>(quarter * 32 + lane);  // row within this CTA's 128 rows
     int it = 0;
     for (int t = cluster; t < total_tiles; t += nclusters, ++it) {
@@ -261,17 +266,21 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
       if (kEpi == kEpiSwigluBwd && valid) {
         // While the MMAs of this tile run, pull this row's h slice (one 128-feature
         // block: 256 contiguous bf16 = 512 B) into L2 so the epilogue loads hit L2.
-        const int f0 = nbk * BN + half * 128;
-        if (f0 < p.N) {
-          const __nv_bfloat16* hrow = static_cast<const __nv_bfloat16*>(p.aux) +
-                                      (static_cast<long long>(p.group_off[g]) + m_half + r) * p.ld_aux + (f0 / 128) * 256;
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], 512;" ::"l"(hrow) : "memory");
+        for (int half = half0; half < half0 + NHALF; ++half) {
+          const int f0 = nbk * BN + half * 128;
+          if (f0 < p.N) {
+            const __nv_bfloat16* hrow = static_cast<const __nv_bfloat16*>(p.aux) +
+                                        (static_cast<long long>(p.group_off[g]) + m_half + r) * p.ld_aux + (f0 / 128) * 256;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], 512;" ::"l"(hrow) : "memory");
+          }
         }
       }
       mbar_wait(&tfull_bar[as], aph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((quarter * 32) << 16) + as * BN;
-      if (valid) {
+      if (valid)
+#pragma unroll 1
+      for (int half = half0; half < half0 + NHALF; ++half) {
         if (kEpi == kEpiF32) {
           const bool empty_k = k_blocks(g) == 0;
           float* out = static_cast<float*>(p.out) + static_cast<long long>(g) * p.out_group_stride +

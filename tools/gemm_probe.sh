@@ -1,4 +1,9 @@
-for pol in 0 5 10 2 8; do for r in 8 16 64; do
-echo "== POL=$pol RASTER=$r"
-POL=$pol RASTER=$r ONLY=up_dgrad,down timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,lts__t_sector_hit_rate.pct --clock-control none -k regex:pair_kernel -s 6 -c 2 --csv python tools/gemm_perf.py 4096 14336 8 4096 2>/dev/null | grep -E "pair_kernel" | awk -F'","' '{print $5, $(NF-2), $(NF-1), $NF}' | sed 's/"//g'
-done; done
+for i in 1 2; do
+echo "== epi warps 8"; PLAIN=1 timeout 300 python tools/gemm_perf.py 4096 14336 8 4096; PLAIN=1 timeout 300 python tools/gemm_perf.py 2048 1408 64 4096
+done
+rm -f paper_2602_11686_b200/lib/obj/grouped_gemm.cu.o paper_2602_11686_b200/lib/obj/debug_capi.cu.o
+FSEP_NVCC_EXTRA="-DFSEP_EPI_WARPS=4" python -c "from paper_2602_11686_b200 import build; build.build()" > /dev/null 2>&1 || echo BUILD FAILED
+python -m pytest tests/test_gpu_gemm.py -x -q 2>&1 | tail -1
+for i in 1 2; do
+echo "== epi warps 4"; PLAIN=1 timeout 300 python tools/gemm_perf.py 4096 14336 8 4096; PLAIN=1 timeout 300 python tools/gemm_perf.py 2048 1408 64 4096
+done
