@@ -16,6 +16,8 @@
 #include <cuda_bf16.h>
 
 #include <cfloat>
+#include <cstdlib>
+#include <string>
 #include <stdexcept>
 
 #include "kernels/fsep_types.cuh"
@@ -26,6 +28,17 @@ namespace fsep {
 namespace {
 
 constexpr int kHC = 64;  // hidden chunk
+
+__device__ __forceinline__ float2 ffma2_rn(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+
 
 template <int TT, int TE>
 __global__ void __launch_bounds__(512) router_gemm_kernel(const __nv_bfloat16* __restrict__ x,
@@ -102,7 +115,12 @@ __global__ void __launch_bounds__(512) router_gemm_kernel(const __nv_bfloat16* _
 #pragma unroll
       for (int i = 0; i < TT; ++i)
 #pragma unroll
-        for (int j = 0; j < TE; ++j) acc[i][j] = __fmaf_rn(xv[i], wv[j], acc[i][j]);
+        for (int j = 0; j < TE; j += 2) {  // FFMA2: two independent chains per instruction
+          const float2 r = ffma2_rn(make_float2(xv[i], xv[i]), make_float2(wv[j], wv[j + 1]),
+                                    make_float2(acc[i][j], acc[i][j + 1]));
+          acc[i][j] = r.x;
+          acc[i][j + 1] = r.y;
+        }
     }
   }
   __syncthreads();
@@ -311,6 +329,120 @@ __global__ void __launch_bounds__(kBlockTokens) router_small_kernel(
   }
 }
 
+// Small-E variant, packed: E_/2 threads per token, each owning the FMA chains of
+// two experts (e0, e0+1) and advancing both with one fma.rn.f32x2 (FFMA2: two
+// independent IEEE fp32 FMAs, so each chain keeps the canonical order).  The
+// router weight sits in shared memory h-major ([H][E_] bf16) so a thread's pair
+// of weights for one h is a single 32-bit load; the token row streams from HBM
+// through a register ring (threads of one token read the same addresses).
+template <int E_>
+__global__ void __launch_bounds__(kBlockTokens * E_ / 2) router_pair_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg, const float* __restrict__ bias, int T,
+    int H, int K, int* __restrict__ topk_idx, float* __restrict__ topk_w, int* __restrict__ intra_rank,
+    int* __restrict__ blk_hist) {
+  constexpr int BT = kBlockTokens, EP = E_ / 2, NT = BT * EP;
+  constexpr int kWords = BT / 32;
+  __shared__ int s_idx[BT][8];
+  __shared__ unsigned s_mask[E_][kWords];
+  __shared__ float s_logit[BT][E_ + 1];
+  extern __shared__ __nv_bfloat162 s_wt[];  // [H][E_/2] pairs: s_wt[h*EP + p] = (w[2p][h], w[2p+1][h])
+  const int tid = threadIdx.x;
+  const int tt = tid / EP, ep = tid % EP;
+  const int t = blockIdx.x * BT + tt;
+  for (int i = tid; i < E_ * kWords; i += NT) (&s_mask[0][0])[i] = 0u;
+  for (int i = tid; i < H * EP; i += NT) {  // transpose the router weight into h-major pairs
+    const int h = i / EP, p = i % EP;
+    s_wt[i] = __halves2bfloat162(wg[static_cast<size_t>(2 * p) * H + h], wg[static_cast<size_t>(2 * p + 1) * H + h]);
+  }
+  __syncthreads();
+  float2 acc = make_float2(0.f, 0.f);
+  const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(min(t, T - 1)) * H);
+  const int pieces = H / 8;
+  constexpr int D = 8;
+  uint4 ring[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) ring[i] = __ldg(xr + i);
+  for (int p0 = 0; p0 < pieces; p0 += D) {
+    uint4 cur[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) cur[i] = ring[i];
+    if (p0 + D < pieces) {
+#pragma unroll
+      for (int i = 0; i < D; ++i) ring[i] = __ldg(xr + p0 + D + i);
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&cur[i]);
+      const __nv_bfloat162* wp = s_wt + static_cast<size_t>(p0 + i) * 8 * EP + ep;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 xf = __bfloat1622float2(b[k]);
+        const float2 w0 = __bfloat1622float2(wp[(2 * k) * EP]);
+        const float2 w1 = __bfloat1622float2(wp[(2 * k + 1) * EP]);
+        acc = ffma2_rn(make_float2(xf.x, xf.x), w0, acc);
+        acc = ffma2_rn(make_float2(xf.y, xf.y), w1, acc);
+      }
+    }
+  }
+  if (t < T) {
+    float a0 = acc.x, a1 = acc.y;
+    if (bias) {
+      a0 = __fadd_rn(a0, __ldg(bias + static_cast<size_t>(t) * E_ + 2 * ep));
+      a1 = __fadd_rn(a1, __ldg(bias + static_cast<size_t>(t) * E_ + 2 * ep + 1));
+    }
+    s_logit[tt][2 * ep] = a0;
+    s_logit[tt][2 * ep + 1] = a1;
+  }
+  __syncthreads();
+  if (tid < BT && blockIdx.x * BT + tid < T) {  // top-k per token (same rule as router_small_kernel)
+    const int u = tid, tu = blockIdx.x * BT + tid;
+    unsigned taken = 0u;
+    float sel_v[8];
+    int sel_e[8];
+    for (int k = 0; k < K; ++k) {
+      float bv = -INFINITY;
+      int be = -1;
+#pragma unroll
+      for (int e = 0; e < E_; ++e)
+        if (!(taken >> e & 1u) && (be < 0 || s_logit[u][e] > bv)) {
+          bv = s_logit[u][e];
+          be = e;
+        }
+      taken |= 1u << be;
+      sel_v[k] = bv;
+      sel_e[k] = be;
+    }
+    float w[8], sum = 0.f;
+    for (int k = 0; k < K; ++k) {
+      w[k] = expf(sel_v[k] - sel_v[0]);
+      sum += w[k];
+    }
+    for (int k = 0; k < K; ++k) {
+      topk_idx[static_cast<size_t>(tu) * K + k] = sel_e[k];
+      topk_w[static_cast<size_t>(tu) * K + k] = w[k] / sum;
+      s_idx[u][k] = sel_e[k];
+      atomicOr(&s_mask[sel_e[k]][u >> 5], 1u << (u & 31));
+    }
+  }
+  __syncthreads();
+  if (tid < BT && blockIdx.x * BT + tid < T) {
+    const int u = tid, tu = blockIdx.x * BT + tid;
+    const int w = u >> 5, l = u & 31;
+    for (int k = 0; k < K; ++k) {
+      const int e = s_idx[u][k];
+      int r = __popc(s_mask[e][w] & ((1u << l) - 1u));
+      for (int ww = 0; ww < w; ++ww) r += __popc(s_mask[e][ww]);
+      intra_rank[static_cast<size_t>(tu) * K + k] = r;
+    }
+  }
+  for (int e = tid; e < E_; e += NT) {
+    int cnt = 0;
+#pragma unroll
+    for (int w = 0; w < kWords; ++w) cnt += __popc(s_mask[e][w]);
+    blk_hist[static_cast<size_t>(blockIdx.x) * E_ + e] = cnt;
+  }
+}
+
 template <int TT, int TE>
 void launch_tiled(const RouterArgs& a, int nblk, cudaStream_t st) {
   const int threads = (kBlockTokens / TT) * (a.E / TE);
@@ -338,7 +470,23 @@ void launch_router(const RouterArgs& a, cudaStream_t st) {
     cudaFuncSetAttribute(router_small_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  if (a.E == 8 && w_bytes <= 200 * 1024)
+  static const bool small = [] {
+    const char* v = std::getenv("FSEP_ROUTER");
+    return v && std::string(v) == "small";
+  }();
+  static bool attr2 = false;
+  if (!attr2) {
+    cudaFuncSetAttribute(router_pair_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(router_pair_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr2 = true;
+  }
+  if (!small && a.E == 8 && w_bytes <= 200 * 1024)
+    router_pair_kernel<8><<<nblk, kBlockTokens * 4, w_bytes, st>>>(a.x, a.wg, a.bias, a.T, a.H, a.K, a.topk_idx,
+                                                                   a.topk_w, a.intra_rank, a.blk_hist);
+  else if (!small && a.E == 16 && w_bytes <= 200 * 1024)
+    router_pair_kernel<16><<<nblk, kBlockTokens * 8, w_bytes, st>>>(a.x, a.wg, a.bias, a.T, a.H, a.K, a.topk_idx,
+                                                                    a.topk_w, a.intra_rank, a.blk_hist);
+  else if (a.E == 8 && w_bytes <= 200 * 1024)
     router_small_kernel<8><<<nblk, kBlockTokens, w_bytes, st>>>(a.x, a.wg, a.bias, a.T, a.H, a.K, a.topk_idx,
                                                                a.topk_w, a.intra_rank, a.blk_hist);
   else if (a.E == 16 && w_bytes <= 200 * 1024)

@@ -49,15 +49,37 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float (&f)[8]) {
 
 // Exclusive scan of per-block counts per expert -> block bases; R row of this
 // rank is published into every rank's R_all (peer stores; local in N=1).
-__global__ void block_scan_kernel(const int* __restrict__ blk_hist, int nblk, int E, int* __restrict__ blk_base,
-                                  PeerTable peers, int rank, int world) {
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    long long acc = 0;
-    for (int b = 0; b < nblk; ++b) {
-      blk_base[static_cast<size_t>(b) * E + e] = static_cast<int>(acc);
-      acc += blk_hist[static_cast<size_t>(b) * E + e];
-    }
-    for (int p = 0; p < world; ++p) peers.R_all[p][static_cast<size_t>(rank) * E + e] = acc;
+// Exclusive scan of the per-block expert counts (block b's base row for expert e
+// among this rank's tokens) and the rank's histogram row R[rank][e], pushed to
+// every rank's R_all.  One CTA per expert: chunked serial sums, a block-wide
+// scan of the chunk totals, then the chunked writes.
+__global__ void __launch_bounds__(256) block_scan_kernel(const int* __restrict__ blk_hist, int nblk, int E,
+                                                         int* __restrict__ blk_base, PeerTable peers, int rank,
+                                                         int world) {
+  __shared__ int s_warp[8];
+  const int e = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (nblk + 255) / 256;
+  const int b0 = min(nblk, tid * per), b1 = min(nblk, b0 + per);
+  int sum = 0;
+  for (int b = b0; b < b1; ++b) sum += blk_hist[static_cast<size_t>(b) * E + e];
+  int inc = sum;  // inclusive warp scan
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  int before = 0;
+  for (int w = 0; w < warp; ++w) before += s_warp[w];
+  int base = before + inc - sum;  // exclusive prefix of this thread's chunk
+  for (int b = b0; b < b1; ++b) {
+    blk_base[static_cast<size_t>(b) * E + e] = base;
+    base += blk_hist[static_cast<size_t>(b) * E + e];
+  }
+  if (tid == 255) {
+    const long long total = static_cast<long long>(before) + inc;
+    for (int p = 0; p < world; ++p) peers.R_all[p][static_cast<size_t>(rank) * E + e] = static_cast<unsigned long long>(total);
   }
 }
 
@@ -569,7 +591,7 @@ __global__ void unpack_grad_kernel(const float* __restrict__ chunk, long long lo
 
 void launch_block_scan(const int* blk_hist, int nblk, int E, int* blk_base, const PeerTable& peers, int rank,
                        int world, cudaStream_t st) {
-  block_scan_kernel<<<1, 128, 0, st>>>(blk_hist, nblk, E, blk_base, peers, rank, world);
+  block_scan_kernel<<<E, 256, 0, st>>>(blk_hist, nblk, E, blk_base, peers, rank, world);
   count_launch();
 }
 
