@@ -1,6 +1,4 @@
 set -x
-python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
 python bench.py --steps 10 --warmup 3 > gpurun_out/b1.json 2> gpurun_out/b1.err; echo b1=$?
-python bench.py --config fine --steps 10 --warmup 3 --no-cpu > gpurun_out/b1_fine.json 2> gpurun_out/b1_fine.err; echo b1f=$?
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_n1.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_l.log 2>&1; echo ncul=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"grouped_gemm|dispatch|combine|unpermute|router|plan_kernel" -s 36 -c 24 -o gpurun_out/prof_full python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_f.log 2>&1; echo ncuf=$?
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"grouped_gemm|dispatch|combine|unpermute|router|plan_kernel|block_scan" -s 40 -c 30 -o gpurun_out/prof_full python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_f.log 2>&1; echo ncuf=$?
