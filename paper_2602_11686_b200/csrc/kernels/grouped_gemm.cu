@@ -119,6 +119,11 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
                a.ldo,        a.out_group_stride, a.out2,    a.ldo2, a.aux, a.ld_aux, a.policy, a.raster,
                a.ready,      a.ready_epoch,      a.ready_n,
                a.row_src,    a.scatter,          a.scatter_rows};
+  static const bool no_tail = [] {
+    const char* v = std::getenv("FSEP_GEMM_NTAIL");
+    return v && std::string(v) == "0";
+  }();
+  if (no_tail) p.policy |= 0x100;
   switch (kind) {
     case GemmKind::kFwdGateUp: launch_pair<false, false, false, kEpiSwigluFwd>(tmA, tmB, p, num_sms, stream); break;
     case GemmKind::kFwdDown: launch_pair<false, false, false, kEpiBf16>(tmA, tmB, p, num_sms, stream); break;

@@ -176,7 +176,10 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
           ready_g = g;
         }
         const int m_half = mb * BM + rank * HALF;   // this CTA's first A row (M-grouped: within the group)
-        const int n_half = nbk * BN + rank * HALF;  // this CTA's first B column
+        // this CTA's first B column; a last N tile with <= 128 live columns runs as
+        // UMMA N=128, each CTA providing 64 columns
+        const bool n_tail = p.N - nbk * BN <= HALF && !(p.policy & 0x100);
+        const int n_half = nbk * BN + rank * (n_tail ? HALF / 2 : HALF);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* sA = smem + s * STAGE_BYTES;
@@ -213,6 +216,7 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
     // ------------------------------------------------------------ MMA issuer (leader CTA)
     if (leader) {
       constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN, kAMN, kBMN);
+      constexpr uint32_t idesc_tail = ptx::idesc_bf16(BM, BN / 2, kAMN, kBMN);  // last N tile with <= 128 columns
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
@@ -225,6 +229,7 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
         mbar_wait(&tempty_bar[as], aph ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + as * BN;
+        const uint32_t id = (p.N - nbk * BN <= HALF && !(p.policy & 0x100)) ? idesc_tail : idesc;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full_bar[s], ph);
           tc_fence_after();
@@ -235,7 +240,7 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
             for (int k = 0; k < BK / 16; ++k) {
               const uint64_t ad = kAMN ? smem_desc(a0 + k * 2048, 8192, 1024) : smem_desc(a0 + k * 32, 16, 1024);
               const uint64_t bd = kBMN ? smem_desc(b0 + k * 2048, 8192, 1024) : smem_desc(b0 + k * 32, 16, 1024);
-              umma_bf16_pair(tmem_d, ad, bd, idesc, (kb | k) ? 1u : 0u);
+              umma_bf16_pair(tmem_d, ad, bd, id, (kb | k) ? 1u : 0u);
             }
             umma_commit_pair(&empty_bar[s], 0x3);
           }

@@ -1,9 +1,1 @@
-for i in 1 2; do
-echo "== epi warps 8"; PLAIN=1 timeout 300 python tools/gemm_perf.py 4096 14336 8 4096; PLAIN=1 timeout 300 python tools/gemm_perf.py 2048 1408 64 4096
-done
-rm -f paper_2602_11686_b200/lib/obj/grouped_gemm.cu.o paper_2602_11686_b200/lib/obj/debug_capi.cu.o
-FSEP_NVCC_EXTRA="-DFSEP_EPI_WARPS=4" python -c "from paper_2602_11686_b200 import build; build.build()" > /dev/null 2>&1 || echo BUILD FAILED
-python -m pytest tests/test_gpu_gemm.py -x -q 2>&1 | tail -1
-for i in 1 2; do
-echo "== epi warps 4"; PLAIN=1 timeout 300 python tools/gemm_perf.py 4096 14336 8 4096; PLAIN=1 timeout 300 python tools/gemm_perf.py 2048 1408 64 4096
-done
+for i in 1 2 3; do for v in 1 0; do echo "== ntail $v"; FSEP_GEMM_NTAIL=$v ONLY=down_dgrad,wgrad_w2,down timeout 300 python tools/gemm_perf.py 2048 1408 64 4096; done; done
