@@ -38,10 +38,10 @@ constexpr int EPI_WARPS = FSEP_EPI_WARPS;  // 8: 4 TMEM lane quarters x 2 column
 static_assert(EPI_WARPS == 8 || EPI_WARPS == 4, "epilogue warps must be 4 or 8");
 constexpr int NHALF = EPI_WARPS == 8 ? 1 : 2;  // column halves per epilogue warp
 constexpr int THREADS = 64 + EPI_WARPS * 32;
-constexpr int MAX_GROUPS = 256;
-constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 512 + (MAX_GROUPS + 1) * 4;
+constexpr int MAX_GROUPS = 128;  // groups = hosted experts (<= kMaxExperts)
+constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 512;  // stages + barriers (tile tables are static smem)
 // SwiGLU-bwd epilogue: per-warp [32 rows][32 fp32] transpose tile (XOR-swizzled float4 slots)
-constexpr int EPI_STAGE_OFF = (STAGES * STAGE_BYTES + 512 + (MAX_GROUPS + 1) * 4 + 127) / 128 * 128;
+constexpr int EPI_STAGE_OFF = STAGES * STAGE_BYTES + 512;
 constexpr int EPI_STAGE_BYTES = EPI_WARPS * 32 * 32 * 4;
 // bf16 epilogues: per-warp [32 rows][64 B] row-piece transpose tile
 constexpr int EPI_STAGE16_BYTES = EPI_WARPS * 32 * 64;
@@ -49,7 +49,8 @@ constexpr int smem_bytes(int epi) {
   return epi == kEpiSwigluBwd ? 1024 + EPI_STAGE_OFF + EPI_STAGE_BYTES
                               : (epi == kEpiF32 ? SMEM_BYTES : 1024 + EPI_STAGE_OFF + EPI_STAGE16_BYTES);
 }
-static_assert(1024 + EPI_STAGE_OFF + EPI_STAGE_BYTES <= 232448, "SwiGLU-bwd staging exceeds shared memory");
+static_assert(1024 + EPI_STAGE_OFF + EPI_STAGE_BYTES + (2 * MAX_GROUPS + 1) * 4 <= 232448,
+              "SwiGLU-bwd staging + tile tables exceed shared memory");
 
 // Coalesced store of a warp's 32 row pieces of 64 B (32 bf16): lane r holds row
 // r's piece in v[0..3]; the pieces are transposed through a 2 KB smem tile
@@ -109,7 +110,8 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-  int* tile_start = reinterpret_cast<int*>(smem + STAGES * STAGE_BYTES + 512);
+  __shared__ int tile_start[MAX_GROUPS + 1];  // first tile of each group (static smem: LDS, not generic loads)
+  __shared__ int group_mbs[MAX_GROUPS];       // M tiles per group
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -124,7 +126,8 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
     int acc = 0;
     for (int g = 0; g < G; ++g) {
       tile_start[g] = acc;
-      acc += kGroupK ? (p.M / BM) * nb : ((p.group_rows[g] + BM - 1) / BM) * nb;
+      group_mbs[g] = kGroupK ? p.M / BM : (p.group_rows[g] + BM - 1) / BM;
+      acc += group_mbs[g] * nb;
     }
     tile_start[G] = acc;
     for (int s = 0; s < STAGES; ++s) {
@@ -148,11 +151,13 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = tile_start[G];
 
+  int gdec = 0;
   auto decode = [&](int t, int& g, int& mb, int& nbk) {
-    g = 0;
-    while (tile_start[g + 1] <= t) ++g;
+    // every role walks its tiles in increasing order: resume the group search
+    while (tile_start[gdec + 1] <= t) ++gdec;
+    g = gdec;
     const int local = t - tile_start[g];
-    const int mbs = kGroupK ? p.M / BM : (p.group_rows[g] + BM - 1) / BM;
+    const int mbs = group_mbs[g];
     raster_tile(local, mbs, nb, p.raster == 0 ? 16 : p.raster, kGroupK, mb, nbk);  // default: 16-tile m-chunks
   };
   auto k_blocks = [&](int g) { return kGroupK ? p.group_rows[g] / BK : p.K / BK; };
