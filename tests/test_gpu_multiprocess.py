@@ -58,3 +58,16 @@ def test_real_multi_gpu(tmp_path, world, E, K, H, F, T, C):
         hist.append(rt.R.astype(np.int64).tolist())
         A = np.array(PP.plan_layout(hist[-1:], topo, params, C, PP.SearchSpec(2, PP.mix_seed(7, 0x6C617972, 0))),
                      dtype=np.uint8)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_real_multi_gpu_modes(world):
+    """Layer chaining (bit-identical to unchained), pure-EP resident experts and
+    local-first routing in real multi-GPU (copy-engine) mode; see mp_worker_modes.py."""
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29518", str(ROOT / "tests" / "mp_worker_modes.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "modes ok" in r.stdout
