@@ -440,11 +440,14 @@ def main():
             b = i % 2
             if i == 0:
                 upload(0)
+            # next step's inputs are queued before this step's work (they wait only for the
+            # step that last used their buffer), so the H2D copies are not stuck behind
+            # this step's copy-engine restore / reduce-scatter pushes
+            upload(i + 1)
             stream.wait_event(ready[b])
             xb, dyb, bb = bufs[b]
             run_step(0, xb, dyb, [[t] for t in bb])
             free[b].record(stream)
-            upload(i + 1)
             m = torch.stack([ys[-1].float().sum(), dxs[0].float().sum()])
             metric_h.copy_(m, non_blocking=True)
 
