@@ -129,9 +129,12 @@ __global__ void plan_kernel(const unsigned long long* __restrict__ R_all, const 
       s_seg_off[d][c] = static_cast<int>(off);
       if (d == rank) {
         pt->slot_expert[c] = e;
-        pt->seg_rows[c] = static_cast<int>(rows);
-        pt->seg_rows_pad[c] = static_cast<int>((rows + 127) / 128 * 128);
         pt->seg_off[c] = static_cast<int>(off);
+        // A segment that does not fit the receive buffer is dropped (the GEMMs see 0
+        // rows; dispatch skips rows past the capacity) and status flags the step.
+        const bool fits = off + (rows + 127) / 128 * 128 <= row_capacity;
+        pt->seg_rows[c] = fits ? static_cast<int>(rows) : 0;
+        pt->seg_rows_pad[c] = fits ? static_cast<int>((rows + 127) / 128 * 128) : 0;
       }
       off += (rows + 127) / 128 * 128;
       ++c;

@@ -12,9 +12,9 @@ from paper_2602_11686_b200.layer import FsepLayer, LayerSpec
 pytestmark = pytest.mark.gpu
 
 
-def _layer(N, E, K, H, F, T, C, seed=0):
+def _layer(N, E, K, H, F, T, C, seed=0, max_recv_rows=0):
     g = torch.Generator().manual_seed(seed)
-    layer = FsepLayer(LayerSpec(E, K, H, F, T, C, world=N, virtual=True))
+    layer = FsepLayer(LayerSpec(E, K, H, F, T, C, world=N, virtual=True, max_recv_rows=max_recv_rows))
     w = {}
     for e in range(E):
         w1 = (torch.randn(F, H, generator=g) / H ** 0.5).bfloat16().cuda()
@@ -99,3 +99,31 @@ def test_extreme_skew_most_experts_idle():
             (-seg) % 128).sum()  # padded total == sum of padded segments
     assert torch.isfinite(y.float()).all() and torch.isfinite(dx.float()).all()
     layer.close()
+
+
+def test_receive_overflow_is_flagged_and_memory_safe():
+    """An undersized receive buffer (max_recv_rows) flags status=1 and drops the
+    segments that do not fit -- no out-of-bounds writes: the device stays healthy
+    and a correctly sized layer afterwards still matches its own eager rerun."""
+    N, E, K, H, F, T, C = 2, 8, 2, 256, 256, 512, 8
+    small = _layer(N, E, K, H, F, T, C, max_recv_rows=256)
+    small.set_layout(PL.even_replication_layout(N, E, C))
+    x, dy, bias = _inputs(N, T, H, E, 1.5, seed=3)
+    y, dx = torch.empty_like(x), torch.empty_like(x)
+    small.forward(x, bias, T, y)
+    small.backward(dy, dx)
+    torch.cuda.synchronize()
+    assert any(small.read("status", v).view(np.int32)[0] == 1 for v in range(N))
+    small.close()
+    ok = _layer(N, E, K, H, F, T, C)
+    ok.set_layout(PL.even_replication_layout(N, E, C))
+    outs = []
+    for _ in range(2):
+        y, dx = torch.empty_like(x), torch.empty_like(x)
+        ok.forward(x, bias, T, y)
+        ok.backward(dy, dx)
+        torch.cuda.synchronize()
+        outs.append((y.clone(), dx.clone()))
+    assert all(ok.read("status", v).view(np.int32)[0] == 0 for v in range(N))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    ok.close()
