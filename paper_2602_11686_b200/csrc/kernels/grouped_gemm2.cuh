@@ -46,8 +46,7 @@ constexpr int EPI_STAGE_BYTES = EPI_WARPS * 32 * 32 * 4;
 // bf16 epilogues: per-warp [32 rows][64 B] row-piece transpose tile
 constexpr int EPI_STAGE16_BYTES = EPI_WARPS * 32 * 64;
 constexpr int smem_bytes(int epi) {
-  return epi == kEpiSwigluBwd ? 1024 + EPI_STAGE_OFF + EPI_STAGE_BYTES
-                              : (epi == kEpiF32 ? SMEM_BYTES : 1024 + EPI_STAGE_OFF + EPI_STAGE16_BYTES);
+  return epi == kEpiSwigluBwd ? 1024 + EPI_STAGE_OFF + EPI_STAGE_BYTES : 1024 + EPI_STAGE_OFF + EPI_STAGE16_BYTES;
 }
 static_assert(1024 + EPI_STAGE_OFF + EPI_STAGE_BYTES + (2 * MAX_GROUPS + 1) * 4 <= 232448,
               "SwiGLU-bwd staging + tile tables exceed shared memory");
@@ -82,7 +81,7 @@ __device__ __forceinline__ void warp_store_rows64(uint32_t stg, const uint4 (&v)
   for (int it = 0; it < 4; ++it) {
     const int rr = it * 8 + sub;
     const uint4 x = lds128(stg + 16 * (rr * 4 + (cg ^ ((rr >> 1) & 3))));
-    __nv_bfloat16* d = dst(rr);
+    auto* d = dst(rr);
     if (d != nullptr) reinterpret_cast<uint4*>(d)[cg] = x;
   }
   __syncwarp();
@@ -292,9 +291,12 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
 #pragma unroll 1
       for (int half = half0; half < half0 + NHALF; ++half) {
         if (kEpi == kEpiF32) {
+          // fp32 rows, stored coalesced: each 32-column chunk goes out as two 64-B row
+          // pieces through the per-warp transpose tile (8 rows x 64 B per store)
           const bool empty_k = k_blocks(g) == 0;
-          float* out = static_cast<float*>(p.out) + static_cast<long long>(g) * p.out_group_stride +
-                       static_cast<long long>(m_half + r) * p.ldo;
+          const uint32_t stg = ptx::smem_u32(smem + EPI_STAGE_OFF) + (warp - 2) * 2048;
+          float* ob = static_cast<float*>(p.out) + static_cast<long long>(g) * p.out_group_stride +
+                      static_cast<long long>(m_half + quarter * 32) * p.ldo;
 #pragma unroll 1
           for (int j = 0; j < 4; ++j) {
             const int c = half * 128 + j * 32;
@@ -307,9 +309,15 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
             } else {
               tmem_ld32(taddr + c, v);
             }
-            float4* dst = reinterpret_cast<float4*>(out + col);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            for (int hh = 0; hh < 2; ++hh) {
+              uint4 o[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                o[q] = make_uint4(__float_as_uint(v[16 * hh + 4 * q]), __float_as_uint(v[16 * hh + 4 * q + 1]),
+                                  __float_as_uint(v[16 * hh + 4 * q + 2]), __float_as_uint(v[16 * hh + 4 * q + 3]));
+              warp_store_rows64(stg, o, [&](int rr) { return ob + rr * p.ldo + col + 16 * hh; });
+            }
           }
         } else if (kEpi == kEpiBf16) {
           const uint32_t stg = ptx::smem_u32(smem + EPI_STAGE_OFF) + (warp - 2) * 2048;
