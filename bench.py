@@ -83,7 +83,7 @@ class ClockSampler:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
                                           "-lms", "50", "-i", str(self.device)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
-            time.sleep(0.5)  # let the sampler start before the timed region begins
+            time.sleep(0.3)  # let the sampler start (idle-only samples are dropped)
         except FileNotFoundError:
             self.proc = None
         return self
@@ -356,12 +356,14 @@ def main():
             ms = t.item()
         return ms
 
-    for i in range(args.warmup):
-        step(i)
-    torch.cuda.synchronize()
-    for layer in layers:
-        layer.stats_reset()
+    # the clock sampler runs from before the warm-up steps to the end of the timed
+    # region, so it sees the GPU under load through the whole measured window
     with ClockSampler(local) as clk:
+        for i in range(args.warmup):
+            step(i)
+        torch.cuda.synchronize()
+        for layer in layers:
+            layer.stats_reset()
         ms = timed(args.steps, lambda i: step(args.warmup + i))
     clocks = clk.result
     sts = [layer.stats() for layer in layers]
