@@ -160,7 +160,7 @@ def run_reference_impl(args, cfg):
     if rank != 0:
         return
     C = args.capacity or default_capacity(cfg["E"], cfg["K"], N)
-    sample = args.cpu_sample or max(64, min(512, int(2.0e12 / (18 * cfg["K"] * cfg["H"] * cfg["F"]))))
+    sample = args.cpu_sample or max(64, min(1024, int(4.0e12 / (18 * cfg["K"] * cfg["H"] * cfg["F"]))))
     ncores = os.cpu_count()
     ts = []
     rate = None
@@ -500,7 +500,7 @@ def main():
     # ---- CPU baseline (rank 0 at N=1 only)
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu:
-        sample = args.cpu_sample or max(64, min(512, int(2.0e12 / (18 * K * H * F))))
+        sample = args.cpu_sample or max(64, min(2048, int(8.0e12 / (18 * K * H * F))))
         rate, detail, secs = cpu_reference_rate(cfg, N, C, args.alpha, sample)
         cpu = {"value": rate, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
                "sample": f"{sample} tokens of the workload through oracle/layer_oracle.py (numpy fp32 BLAS, "
