@@ -38,7 +38,16 @@ void check_encode(CUresult r, const char* what) {
 }  // namespace
 
 uint64_t launches_issued() { return g_launches.load(); }
-void count_launch(int n) { g_launches += static_cast<uint64_t>(n); }
+// Every launcher calls this right after its launch: count it, and surface launch
+// errors (bad configuration, shared-memory limits) at the call that caused them.
+void count_launch(int n) {
+  g_launches += static_cast<uint64_t>(n);
+  const cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw std::runtime_error(std::string("kernel launch failed: ") + cudaGetErrorString(e));
+  }
+}
 
 CUtensorMap make_tmap_2d(const void* base, uint64_t inner, uint64_t outer, uint64_t pitch_elems, uint32_t box_inner,
                          uint32_t box_outer) {
