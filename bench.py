@@ -455,7 +455,7 @@ def main():
             xb, dyb, bb = bufs[b]
             run_step(0, xb, dyb, [[t] for t in bb])
             free[b].record(stream)
-            m = torch.stack([ys[-1].float().sum(), dxs[0].float().sum()])
+            m = torch.stack([ys[-1].sum(dtype=torch.float32), dxs[0].sum(dtype=torch.float32)])
             metric_h.copy_(m, non_blocking=True)
 
         for i in range(args.warmup):
