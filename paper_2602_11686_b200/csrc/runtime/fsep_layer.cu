@@ -140,6 +140,7 @@ extern "C" struct mp_fsep_layer {
   bool local_first = false;    // MP_FSEP_FLAG_LOCAL_FIRST (non-parity routing variant)
   mp_fsep_layer* next = nullptr;  // chained next layer: its restore is issued after this layer's dispatch
   bool prefetched = false;        // this layer's restore for the coming forward is already in flight
+  bool restore_split = true;      // push slot 0 before dispatch, the rest after (FSEP_RESTORE_SPLIT=0: all before)
   // graph
   cudaGraphExec_t graph = nullptr;
   const void* graph_key[5] = {};
@@ -396,17 +397,20 @@ void snapshot_layout(Layer& L, cudaStream_t st) {
 // restored slot of each rank that hosts it (own slots first), and a flag written
 // into the destination's memory after each copy releases that (slot, source)
 // pair to the destination's gate-up GEMM producer.  Ordered after `st`'s work.
-void push_restore(Layer& L, cudaStream_t st) {
+// Slots [c0, c1) of every destination; c0 == 0 opens a new restore epoch.
+void push_restore(Layer& L, cudaStream_t st, int c0 = 0, int c1 = kMaxExperts) {
   const int E = L.E, N = L.N;
   Rank& r = L.ranks[0];
-  ++L.restore_epoch;
+  if (c0 == 0) {
+    ++L.restore_epoch;
+    mark(L, st, kPhRestoreBegin);
+  }
   CK(cudaEventRecord(L.ev_fork, st));
-  mark(L, st, kPhRestoreBegin);
   for (int q = 0; q < N; ++q) {
     const int d = (r.rank + q) % N;
     const std::vector<int> theirs = hosted_experts(L.cur_layout, E, N, d);
     CK(cudaStreamWaitEvent(L.ce[d], L.ev_fork, 0));
-    for (int c = 0; c < static_cast<int>(theirs.size()); ++c) {
+    for (int c = c0; c < std::min(c1, static_cast<int>(theirs.size())); ++c) {
       CK(cudaMemcpyAsync(L.peer_restored[d] + static_cast<long long>(c) * L.flat + static_cast<long long>(r.rank) * L.S,
                          r.shard + static_cast<long long>(theirs[c]) * L.S, static_cast<size_t>(L.S) * 2,
                          cudaMemcpyDeviceToDevice, L.ce[d]));
@@ -446,7 +450,9 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   barrier(L, st);
   mark(L, st, kPhParamBarrier);
   if (restore && ce) {
-    if (!prefetched) push_restore(L, st);
+    // only slot 0 now; the other slots after dispatch, so the restore does not
+    // compete with the dispatch for NVLink (slot 0 is what the GEMMs need first)
+    if (!prefetched) push_restore(L, st, 0, L.restore_split ? 1 : kMaxExperts);
   } else if (restore) {
     CK(cudaEventRecord(L.ev_fork, st));
     CK(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
@@ -495,6 +501,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
                                  r.rank},
                     st);
   mark(L, st, kPhDispatch);
+  if (restore && ce && !prefetched && L.restore_split) push_restore(L, st, 1, kMaxExperts);
   // Fig.5 schedule: the next layer's expert restore travels on the copy engines
   // while this layer's expert MLP runs (safe: every rank has passed this step's
   // parameter barrier, so all of the previous step's work is complete).
@@ -713,6 +720,7 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     L->virt = d.virtual_ranks != 0 || L->N == 1;
     L->resident = (d.flags & MP_FSEP_FLAG_RESIDENT_EXPERTS) != 0;
     L->local_first = (d.flags & MP_FSEP_FLAG_LOCAL_FIRST) != 0;
+    if (const char* v = std::getenv("FSEP_RESTORE_SPLIT")) L->restore_split = std::string(v) != "0";
     require(!L->resident || d.n_experts == d.world * d.capacity,
             "resident-expert (pure EP) mode needs E == N*C (one host per expert)");
     const long long worst = static_cast<long long>(d.max_tokens) * d.top_k * L->N + 128LL * L->C;
