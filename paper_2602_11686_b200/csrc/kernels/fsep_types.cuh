@@ -33,6 +33,11 @@ struct PeerTable {
   __nv_bfloat16* dy_rows[kMaxRanks];
   __nv_bfloat16* tok_rows[kMaxRanks];  // [T_max*K][H] on each rank (y, later reused for dX)
   int* row_src[kMaxRanks];             // [row_capacity] origin of each receive row on each rank
+  // Token de-duplication (K >= 4, N > 1): a token row crosses NVLink once per
+  // destination device into stage[dst][src][t]; the destination expands it into
+  // its slot rows (x rows in the forward, w_k-scaled dY rows in the backward).
+  __nv_bfloat16* stage[kMaxRanks];     // [N][T_max][H] on each rank (null: no de-duplication)
+  float* row_w[kMaxRanks];             // [row_capacity] gate weight w_k of each receive row
   unsigned long long* R_all[kMaxRanks];  // [N][E] on each rank
   float* grad_full[kMaxRanks];           // [C][3HF] restored-expert grads on each rank
   const __nv_bfloat16* shard[kMaxRanks]; // [E][S] FSEP shards on each rank

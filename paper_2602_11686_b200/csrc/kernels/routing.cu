@@ -235,7 +235,8 @@ template <int CH>
 __global__ void __launch_bounds__(kDispatchWarps * 32) dispatch_tma_kernel(
     const __nv_bfloat16* __restrict__ x, int T, int K, int E, const int* __restrict__ topk_idx,
     const int* __restrict__ intra_rank, const int* __restrict__ blk_base, const PlanTables* __restrict__ pt,
-    PeerTable peers, uint32_t* __restrict__ slot_dst, int src_rank) {
+    PeerTable peers, uint32_t* __restrict__ slot_dst, int src_rank, const float* __restrict__ topk_w, int T_max,
+    bool dedupe) {
   using namespace ptx;
   constexpr int H = CH * 256;
   constexpr uint32_t RB = H * 2;
@@ -264,6 +265,7 @@ __global__ void __launch_bounds__(kDispatchWarps * 32) dispatch_tma_kernel(
     if (t >= T) break;
     // lane k resolves slot k's destination (same rule as dispatch_kernel)
     unsigned long long dst = 0;
+    int rdev = -1;  // de-duplicated remote destination device of slot k
     if (lane < K) {
       const int k = lane;
       const int e = topk_idx[static_cast<size_t>(t) * K + k];
@@ -275,17 +277,32 @@ __global__ void __launch_bounds__(kDispatchWarps * 32) dispatch_tma_kernel(
       slot_dst[static_cast<size_t>(t) * K + k] = (static_cast<uint32_t>(d) << 24) | static_cast<uint32_t>(row);
       if (static_cast<uint64_t>(row) < peers.row_capacity) {
         peers.row_src[d][row] = (src_rank << kRowSrcShift) | (t * K + k);
-        dst = reinterpret_cast<unsigned long long>(peers.x_rows[d] + static_cast<size_t>(row) * H);
+        if (dedupe) {
+          peers.row_w[d][row] = topk_w[static_cast<size_t>(t) * K + k];
+          if (d != src_rank) rdev = d;
+        }
+        if (rdev < 0) dst = reinterpret_cast<unsigned long long>(peers.x_rows[d] + static_cast<size_t>(row) * H);
       }
     }
     unsigned long long dk[8];
+    int rk[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) dk[k] = __shfl_sync(0xffffffffu, dst, k);
+    for (int k = 0; k < 8; ++k) {
+      dk[k] = __shfl_sync(0xffffffffu, dst, k);
+      rk[k] = __shfl_sync(0xffffffffu, rdev, k);
+    }
     if (lane == 0) {
       mbar_wait(&bar[j % NB], (j / NB) & 1);
       const uint8_t* src = buf + static_cast<size_t>(j % NB) * RB;
-      for (int k = 0; k < K; ++k)
+      for (int k = 0; k < K; ++k) {
         if (dk[k]) bulk_s2g(reinterpret_cast<void*>(dk[k]), src, RB);
+        if (rk[k] >= 0) {  // once per remote device: the token row into its staging area
+          bool seen = false;
+          for (int q = 0; q < k; ++q) seen |= rk[q] == rk[k];
+          if (!seen)
+            bulk_s2g(peers.stage[rk[k]] + (static_cast<size_t>(src_rank) * T_max + t) * H, src, RB);
+        }
+      }
       bulk_commit();
       if (j >= 1) {  // buffer of token j-1 is free once its stores have read it
         bulk_wait_read<1>();
@@ -355,7 +372,8 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(int T, int K, const __
                                                           const __nv_bfloat16* __restrict__ tok_rows,
                                                           const uint32_t* __restrict__ slot_dst, PeerTable peers,
                                                           float* __restrict__ dl, __nv_bfloat16* __restrict__ dl_dense,
-                                                          int* __restrict__ rw_rows, int* __restrict__ rw_off) {
+                                                          int* __restrict__ rw_rows, int* __restrict__ rw_off,
+                                                          int src_rank, int T_max, bool dedupe) {
   constexpr int H = CH * 256;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const int tpad = (T + 127) / 128 * 128;
@@ -370,16 +388,33 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(int T, int K, const __
   const uint4* g = reinterpret_cast<const uint4*>(dout + static_cast<size_t>(t) * H);
   float dot[8];
   float w[8];
+  // per slot: write the scaled dY row directly (local, or every slot without
+  // de-duplication), or -- de-duplicated remote device, first slot on it -- send
+  // the raw dout row once into that device's staging area (expanded there)
+  bool direct[8], first[8];
+  int dev[8];
   for (int k = 0; k < K; ++k) {
     dot[k] = 0.f;
     w[k] = topk_w[static_cast<size_t>(t) * K + k];
+    const uint32_t code = slot_dst[static_cast<size_t>(t) * K + k];
+    dev[k] = static_cast<int>(code >> 24);
+    const bool valid = (code & 0xFFFFFFu) < peers.row_capacity;  // dropped slots (receive overflow) are skipped
+    const bool remote = dedupe && dev[k] != src_rank;
+    direct[k] = valid && !remote;
+    bool seen = false;
+    for (int q = 0; q < k; ++q) seen |= first[q] && dev[q] == dev[k];
+    first[k] = valid && remote && !seen;
   }
 #pragma unroll
   for (int c0 = 0; c0 < CH; c0 += 4) {
     float gf[4][8];
+    uint4 graw[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c)
-      if (c0 + c < CH) bf16x8_to_f32(__ldg(g + (c0 + c) * 32 + lane), gf[c]);
+      if (c0 + c < CH) {
+        graw[c] = __ldg(g + (c0 + c) * 32 + lane);
+        bf16x8_to_f32(graw[c], gf[c]);
+      }
     for (int k = 0; k < K; ++k) {
       const uint32_t code = slot_dst[static_cast<size_t>(t) * K + k];
       const uint4* y = reinterpret_cast<const uint4*>(tok_rows + (static_cast<size_t>(t) * K + k) * H);
@@ -398,7 +433,13 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(int T, int K, const __
           dot[k] = __fmaf_rn(gf[c][j], f[j], dot[k]);
           s[j] = w[k] * gf[c][j];
         }
-        dy[(c0 + c) * 32 + lane] = f32_to_bf16x8(s);
+        if (direct[k]) dy[(c0 + c) * 32 + lane] = f32_to_bf16x8(s);
+      }
+      if (first[k]) {
+        uint4* st = reinterpret_cast<uint4*>(peers.stage[dev[k]] + (static_cast<size_t>(src_rank) * T_max + t) * H);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c0 + c < CH) st[(c0 + c) * 32 + lane] = graw[c];
       }
     }
   }
@@ -414,6 +455,46 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(int T, int K, const __
       dl[static_cast<size_t>(t) * K + k] = v;
       dl_dense[static_cast<size_t>(t) * kDLCols + topk_idx[static_cast<size_t>(t) * K + k]] = __float2bfloat16_rn(v);
     }
+}
+
+// ------------------------------------------------------------- expansion
+// De-duplicated transfers land once per (source, token) in stage[src][t]; every
+// receive row whose source is another rank copies its token row from there
+// (forward: x rows), or -- with row weights -- writes bf16(w_k * dout) (backward:
+// dY rows, the same fp32 product combine_bwd forms for local slots).
+template <int CH>
+__global__ void __launch_bounds__(256) expand_rows_kernel(const PlanTables* __restrict__ pt, long long capacity,
+                                                          const int* __restrict__ row_src,
+                                                          const __nv_bfloat16* __restrict__ stage,
+                                                          const float* __restrict__ row_w, int rank, int K,
+                                                          int T_max, __nv_bfloat16* __restrict__ rows) {
+  constexpr int H = CH * 256;
+  const int lane = threadIdx.x & 31;
+  const long long n = min(static_cast<long long>(pt->total_rows), capacity);
+  for (long long r = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < n;
+       r += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
+    const int code = row_src[r];
+    if (code < 0) continue;
+    const int s = code >> kRowSrcShift;
+    if (s == rank) continue;  // written directly by the local dispatch / combine-bwd
+    const int t = (code & ((1 << kRowSrcShift) - 1)) / K;
+    const uint4* src = reinterpret_cast<const uint4*>(stage + (static_cast<size_t>(s) * T_max + t) * H);
+    uint4* dst = reinterpret_cast<uint4*>(rows + static_cast<size_t>(r) * H);
+    if (row_w == nullptr) {
+#pragma unroll
+      for (int c = 0; c < CH; ++c) dst[c * 32 + lane] = src[c * 32 + lane];
+    } else {
+      const float w = row_w[r];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        float f[8], o[8];
+        bf16x8_to_f32(src[c * 32 + lane], f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = w * f[j];
+        dst[c * 32 + lane] = f32_to_bf16x8(o);
+      }
+    }
+  }
 }
 
 // ----------------------------------------------------------- unpermute bwd
@@ -633,7 +714,8 @@ void launch_dispatch(const DispatchArgs& a, cudaStream_t st) {
       }
       const int blocks = std::min(sms, (a.T + kDispatchWarps - 1) / kDispatchWarps);
       dispatch_tma_kernel<CH><<<blocks, kDispatchWarps * 32, smem, st>>>(
-          a.x, a.T, a.K, a.E, a.topk_idx, a.intra_rank, a.blk_base, a.pt, a.peers, a.slot_dst, a.rank);
+          a.x, a.T, a.K, a.E, a.topk_idx, a.intra_rank, a.blk_base, a.pt, a.peers, a.slot_dst, a.rank, a.topk_w,
+          a.T_max, a.dedupe);
     });
   } else {
     FSEP_CH_SWITCH(a.H / 256, dispatch_kernel<CH><<<(a.T + 7) / 8, 256, 0, st>>>(
@@ -652,12 +734,14 @@ void launch_combine(int T, int H, int K, const float* topk_w, const __nv_bfloat1
 
 void launch_combine_bwd(int T, int H, int K, const __nv_bfloat16* dout, const float* topk_w, const int* topk_idx,
                         const __nv_bfloat16* tok_rows, const uint32_t* slot_dst, const PeerTable& peers, float* dl,
-                        __nv_bfloat16* dl_dense, int* rw_rows, int* rw_off, cudaStream_t st) {
+                        __nv_bfloat16* dl_dense, int* rw_rows, int* rw_off, int rank, int T_max, bool dedupe,
+                        cudaStream_t st) {
   if (T == 0) return;
   const size_t tpad = (static_cast<size_t>(T) + 127) / 128 * 128;
   cudaMemsetAsync(dl_dense, 0, tpad * kDLCols * sizeof(__nv_bfloat16), st);
   FSEP_CH_SWITCH(H / 256, combine_bwd_kernel<CH><<<(T + 7) / 8, 256, 0, st>>>(
-                              T, K, dout, topk_w, topk_idx, tok_rows, slot_dst, peers, dl, dl_dense, rw_rows, rw_off));
+                              T, K, dout, topk_w, topk_idx, tok_rows, slot_dst, peers, dl, dl_dense, rw_rows, rw_off,
+                              rank, T_max, dedupe));
   count_launch();
 }
 
@@ -665,6 +749,14 @@ void launch_unpermute_bwd(int T, int H, int K, const int* topk_idx, const float*
                           const __nv_bfloat16* wg, __nv_bfloat16* dx, cudaStream_t st) {
   if (T == 0) return;
   FSEP_CH_SWITCH(H / 256, unpermute_bwd_kernel<CH><<<(T + 7) / 8, 256, 0, st>>>(T, K, topk_idx, dl, tok_rows, wg, dx));
+  count_launch();
+}
+
+void launch_expand_rows(const PlanTables* pt, long long capacity, const int* row_src, const __nv_bfloat16* stage,
+                        const float* row_w, int rank, int H, int K, int T_max, __nv_bfloat16* rows, int num_sms,
+                        cudaStream_t st) {
+  FSEP_CH_SWITCH(H / 256, expand_rows_kernel<CH><<<num_sms * 8, 256, 0, st>>>(pt, capacity, row_src, stage, row_w,
+                                                                             rank, K, T_max, rows));
   count_launch();
 }
 

@@ -30,6 +30,9 @@ struct DispatchArgs {
   PeerTable peers;
   uint32_t* slot_dst;
   int rank;  // source rank (row_src codes)
+  const float* topk_w = nullptr;  // de-duplication: gate weights recorded per receive row
+  int T_max = 0;
+  bool dedupe = false;            // remote destinations get each token row once (PeerTable::stage)
 };
 
 void launch_router(const RouterArgs& a, cudaStream_t st);
@@ -44,7 +47,14 @@ void launch_combine(int T, int H, int K, const float* topk_w, const __nv_bfloat1
                     cudaStream_t st);
 void launch_combine_bwd(int T, int H, int K, const __nv_bfloat16* dout, const float* topk_w, const int* topk_idx,
                         const __nv_bfloat16* tok_rows, const uint32_t* slot_dst, const PeerTable& peers, float* dl,
-                        __nv_bfloat16* dl_dense, int* rw_rows, int* rw_off, cudaStream_t st);
+                        __nv_bfloat16* dl_dense, int* rw_rows, int* rw_off, int rank, int T_max, bool dedupe,
+                        cudaStream_t st);
+// De-duplicated transfers: expand stage[src][t] into this rank's receive rows
+// (row_w == nullptr: copy x rows; else dY rows = bf16(row_w[r] * stage row)).
+void launch_expand_rows(const PlanTables* pt, long long capacity, const int* row_src, const __nv_bfloat16* stage,
+                        const float* row_w, int rank, int H, int K, int T_max, __nv_bfloat16* rows, int num_sms,
+                        cudaStream_t st);
+bool use_tma_dispatch();
 void launch_unpermute_bwd(int T, int H, int K, const int* topk_idx, const float* dl, const __nv_bfloat16* tok_rows,
                           const __nv_bfloat16* wg, __nv_bfloat16* dx, cudaStream_t st);
 int router_wgrad_splits(int T);

@@ -74,6 +74,8 @@ struct Rank {
   size_t arena_bytes = 0;
   __nv_bfloat16 *x_rows = nullptr, *dy_rows = nullptr, *tok_rows = nullptr;
   int* row_src = nullptr;
+  __nv_bfloat16* stage = nullptr;  // de-duplication: [N][T_max][H] token rows from each source
+  float* row_w = nullptr;          // de-duplication: [cap] w_k of each receive row
   unsigned long long* R_all = nullptr;
   float* grad_full = nullptr;
   __nv_bfloat16* shard = nullptr;
@@ -138,6 +140,7 @@ extern "C" struct mp_fsep_layer {
   bool resident = false;       // MP_FSEP_FLAG_RESIDENT_EXPERTS: pure EP (no per-step restore / RS)
   bool restore_dirty = true;   // resident mode: hosted experts must be (re)restored
   bool local_first = false;    // MP_FSEP_FLAG_LOCAL_FIRST (non-parity routing variant)
+  bool dedupe = false;         // token rows cross NVLink once per destination device (K >= 4)
   mp_fsep_layer* next = nullptr;  // chained next layer: its restore is issued after this layer's dispatch
   bool prefetched = false;        // this layer's restore for the coming forward is already in flight
   bool restore_split = true;      // push slot 0 before dispatch, the rest after (FSEP_RESTORE_SPLIT=0: all before)
@@ -256,6 +259,10 @@ void allocate_rank(Layer& L, Rank& r) {
   acc(cap * H * 2);  // dy_rows
   acc(T * K * H * 2);  // tok_rows
   acc(cap * 4);      // row_src
+  if (L.dedupe) {
+    acc(N * T * H * 2);  // stage
+    acc(cap * 4);        // row_w
+  }
   acc(N * E * 8);    // R_all
   acc(C * flat * 4);  // grad_full
   acc(E * S * 2);    // shard
@@ -274,6 +281,10 @@ void allocate_rank(Layer& L, Rank& r) {
   r.dy_rows = ca.take<__nv_bfloat16>(cap * H);
   r.tok_rows = ca.take<__nv_bfloat16>(T * K * H);
   r.row_src = ca.take<int>(cap);
+  if (L.dedupe) {
+    r.stage = ca.take<__nv_bfloat16>(N * T * H);
+    r.row_w = ca.take<float>(cap);
+  }
   r.R_all = ca.take<unsigned long long>(N * E);
   r.grad_full = ca.take<float>(C * flat);
   r.shard = ca.take<__nv_bfloat16>(E * S);
@@ -344,6 +355,8 @@ void finish_peers(Layer& L) {
       L.peers.dy_rows[p] = r.dy_rows;
       L.peers.tok_rows[p] = r.tok_rows;
       L.peers.row_src[p] = r.row_src;
+      L.peers.stage[p] = r.stage;
+      L.peers.row_w[p] = r.row_w;
       L.peers.R_all[p] = r.R_all;
       L.peers.grad_full[p] = r.grad_full;
       L.peers.shard[p] = r.shard;
@@ -498,7 +511,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   }
   for (Rank& r : L.ranks)
     launch_dispatch(DispatchArgs{r.x_in, T, H, K, E, r.topk_idx, r.intra_rank, r.blk_base, r.pt, L.peers, r.slot_dst,
-                                 r.rank},
+                                 r.rank, r.topk_w, L.T_max, L.dedupe},
                     st);
   mark(L, st, kPhDispatch);
   if (restore && ce && !prefetched && L.restore_split) push_restore(L, st, 1, kMaxExperts);
@@ -512,6 +525,9 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
     nx.prefetched = true;
   }
   barrier(L, st);
+  if (L.dedupe)  // token rows that crossed NVLink once per device -> this rank's slot rows
+    for (Rank& r : L.ranks)
+      launch_expand_rows(r.pt, L.cap, r.row_src, r.stage, nullptr, r.rank, H, K, L.T_max, r.x_rows, L.num_sms, st);
   mark(L, st, kPhDispatchBarrier);
   // 5. expert FFN on the restored experts
   if (restore && !ce) CK(cudaStreamWaitEvent(st, L.ev_restored, 0));
@@ -565,12 +581,15 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   for (size_t v = 0; v < L.ranks.size(); ++v) {
     Rank& r = L.ranks[v];
     launch_combine_bwd(T, H, K, dy + (L.virt ? static_cast<long long>(v) * TH : 0), r.topk_w, r.topk_idx, r.tok_rows,
-                       r.slot_dst, L.peers, r.dl, r.dl_dense, r.rw_rows, r.rw_off, st);
+                       r.slot_dst, L.peers, r.dl, r.dl_dense, r.rw_rows, r.rw_off, r.rank, L.T_max, L.dedupe, st);
     launch_router_wgrad(r.x_in, T, H, E, r.dl_dense, L.T_max, r.rw_rows, r.rw_off, r.dwg_partial, r.dwg, L.num_sms,
                         st);
   }
   mark(L, st, kPhCombineBwd);
   barrier(L, st);
+  if (L.dedupe)  // dout rows that crossed NVLink once per device -> w_k-scaled dY slot rows
+    for (Rank& r : L.ranks)
+      launch_expand_rows(r.pt, L.cap, r.row_src, r.stage, r.row_w, r.rank, H, K, L.T_max, r.dy_rows, L.num_sms, st);
   mark(L, st, kPhCombineBwdBarrier);
   CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][2], st));
   // Weight gradients first: in copy-engine mode their reduce-scatter pushes run
@@ -720,6 +739,10 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     L->virt = d.virtual_ranks != 0 || L->N == 1;
     L->resident = (d.flags & MP_FSEP_FLAG_RESIDENT_EXPERTS) != 0;
     L->local_first = (d.flags & MP_FSEP_FLAG_LOCAL_FIRST) != 0;
+    // de-duplicated token transfers pay off when a token has several slots per
+    // device (top-k >= 4); FSEP_DEDUPE=0/1 overrides
+    L->dedupe = L->N > 1 && d.top_k >= 4 && use_tma_dispatch();
+    if (const char* v = std::getenv("FSEP_DEDUPE")) L->dedupe = L->N > 1 && std::string(v) != "0" && use_tma_dispatch();
     if (const char* v = std::getenv("FSEP_RESTORE_SPLIT")) L->restore_split = std::string(v) != "0";
     require(!L->resident || d.n_experts == d.world * d.capacity,
             "resident-expert (pure EP) mode needs E == N*C (one host per expert)");
@@ -858,6 +881,10 @@ mp_status mp_fsep_layer_connect(mp_fsep_layer* L, const void* all_handles, const
       L->peers.dy_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.dy_rows));
       L->peers.tok_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.tok_rows));
       L->peers.row_src[p] = reinterpret_cast<int*>(base + off(me.row_src));
+      if (L->dedupe) {
+        L->peers.stage[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.stage));
+        L->peers.row_w[p] = reinterpret_cast<float*>(base + off(me.row_w));
+      }
       if (L->ce_mode) {
         L->peer_restored[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.restored));
         L->peer_ready[p] = reinterpret_cast<unsigned*>(base + off(me.ready));
