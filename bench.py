@@ -404,18 +404,6 @@ def main():
                 "frac_of_burst": round(gemm_tflops / burst, 4),
                 "step_frac": round(value / N * flop_tok / (sustained * 1e12), 4)}
 
-    # ---- static-EP comparison (same kernels, static_ep_layout at the same C)
-    static = None
-    if N > 1 and args.layout == "laer" and not args.no_static:
-        for layer in layers:
-            layer.detach_planner()
-            layer.set_layout(PL.static_ep_layout(N, E, C))
-        for i in range(args.warmup):
-            step(i)
-        sms = timed(args.steps, lambda i: step(args.warmup + i))
-        static = {"value": N * T / (sms * 1e-3), "ms_per_step": sms, "layout": "static_ep_layout(N,E,C)",
-                  "speedup_laer_over_static": round(sms / ms, 4)}
-
     # ---- end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -467,6 +455,18 @@ def main():
                "ms_per_step": ems,
                "note": "x, dy, routing bias H2D from pinned host memory every step (double-buffered copy stream) "
                        "+ [sum y, sum dx] D2H per step, inside the timed region"}
+
+    # ---- static-EP comparison (same kernels, static_ep_layout at the same C)
+    static = None
+    if N > 1 and args.layout == "laer" and not args.no_static:
+        for layer in layers:
+            layer.detach_planner()
+            layer.set_layout(PL.static_ep_layout(N, E, C))
+        for i in range(args.warmup):
+            step(i)
+        sms = timed(args.steps, lambda i: step(args.warmup + i))
+        static = {"value": N * T / (sms * 1e-3), "ms_per_step": sms, "layout": "static_ep_layout(N,E,C)",
+                  "speedup_laer_over_static": round(sms / ms, 4)}
 
     # ---- pure expert parallelism: C = E/N, one host per expert, experts
     # resident across steps, no restore and no gradient reduce-scatter -- same kernels
