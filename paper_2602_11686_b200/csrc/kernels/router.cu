@@ -98,19 +98,16 @@ __global__ void __launch_bounds__(512) router_gemm_kernel(const __nv_bfloat16* _
 #pragma unroll 8
     for (int h = 0; h < kHC; ++h) {
       float xv[TT], wv[TE];
-      if constexpr (TT == 4) {
-        const float4 v = *reinterpret_cast<const float4*>(s_x + h * BT + tg * TT);
-        xv[0] = v.x, xv[1] = v.y, xv[2] = v.z, xv[3] = v.w;
-      } else {
+      static_assert(TT % 4 == 0 && TE % 4 == 0, "register tile must be float4-aligned");
 #pragma unroll
-        for (int i = 0; i < TT; ++i) xv[i] = s_x[h * BT + tg * TT + i];
+      for (int i = 0; i < TT; i += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(s_x + h * BT + tg * TT + i);
+        xv[i] = v.x, xv[i + 1] = v.y, xv[i + 2] = v.z, xv[i + 3] = v.w;
       }
-      if constexpr (TE == 4) {
-        const float4 v = *reinterpret_cast<const float4*>(s_w + h * E + eg * TE);
-        wv[0] = v.x, wv[1] = v.y, wv[2] = v.z, wv[3] = v.w;
-      } else {
 #pragma unroll
-        for (int j = 0; j < TE; ++j) wv[j] = s_w[h * E + eg * TE + j];
+      for (int j = 0; j < TE; j += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(s_w + h * E + eg * TE + j);
+        wv[j] = v.x, wv[j + 1] = v.y, wv[j + 2] = v.z, wv[j + 3] = v.w;
       }
 #pragma unroll
       for (int i = 0; i < TT; ++i)
@@ -493,7 +490,16 @@ void launch_router(const RouterArgs& a, cudaStream_t st) {
     router_small_kernel<16><<<nblk, kBlockTokens, w_bytes, st>>>(a.x, a.wg, a.bias, a.T, a.H, a.K, a.topk_idx,
                                                                 a.topk_w, a.intra_rank, a.blk_hist);
   else
-    launch_tiled<4, 4>(a, nblk, st);  // 16 x E/4 threads, register-tiled
+  {
+    static const int tile = [] {
+      const char* v = std::getenv("FSEP_ROUTER_TILE");
+      return v ? std::atoi(v) : 4;  // 8x8 tiles measured slower (0.66 vs 0.57 ms, fine config)
+    }();
+    if (tile == 8 && a.E % 8 == 0)
+      launch_tiled<8, 8>(a, nblk, st);  // 8 x E/8 threads, 8x8 register tiles (half the smem traffic per FMA)
+    else
+      launch_tiled<4, 4>(a, nblk, st);  // 16 x E/4 threads
+  }
   count_launch();
 }
 
