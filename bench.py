@@ -368,6 +368,8 @@ def main():
     clocks = clk.result
     sts = [layer.stats() for layer in layers]
     phases = layers[0].phase_ms() if os.environ.get("FSEP_PHASE_TIMING") == "1" else None
+    if phases:
+        phases["fwd_gemms"] = round(phases["fwd_gemm_gateup"] + phases["fwd_gemm_down"], 4)
     comm = token_kernel_bandwidth(phases, layers[0], PL, N, rank, T, K, H) if phases else None
     per_rank = None
     if world > 1 and phases:
@@ -375,7 +377,7 @@ def main():
         allp = [None] * world
         rows = int(layers[0].read("total_rows").view(np.int32)[0])
         dist.all_gather_object(allp, {"phases": phases, "gemm_ms": sum(s_["gemm_ms"] for s_ in sts), "rows": rows})
-        keys = ["router_scan", "dispatch", "fwd_gemms", "fwd_barrier", "combine_bwd_router_wgrad", "bwd_gemms",
+        keys = ["router_scan", "dispatch", "fwd_gemm_gateup", "fwd_gemm_down", "fwd_gemms", "fwd_barrier", "combine_bwd_router_wgrad", "bwd_gemms",
                 "rs_sum_barrier", "step_total"]
         per_rank = {k: [round(a["phases"].get(k, 0.0), 3) for a in allp] for k in keys}
         per_rank["gemm_ms"] = [round(a["gemm_ms"], 3) for a in allp]

@@ -180,6 +180,7 @@ enum Phase : int {
   kPhDispatch,
   kPhDispatchBarrier,
   kPhRestoreWait,
+  kPhFwdGateUp,  // gate-up GEMM done (the down GEMM follows)
   kPhFwdGemm,
   kPhFwdGemmBarrier,
   kPhCombine,
@@ -547,6 +548,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
     g.out2 = r.act;
     g.ldo2 = F;
     gemm(L, GemmKind::kFwdGateUp, r.tm_x_k, r.tm_w13_k, r.tm_w13_k128, g, st);
+    if (&r == &L.ranks.back()) mark(L, st, kPhFwdGateUp);
     GroupedGemmArgs g2 = g;
     g2.N = H;
     g2.K = F;

@@ -164,14 +164,14 @@ class FsepLayer:
         return {"kernel_launches": n.value, "gemm_ms": ms.value, "gemm_flops": fl.value}
 
     PHASES = ["param_barrier", "router_scan", "R_barrier", "plan", "dispatch", "dispatch_barrier", "restore_wait",
-              "fwd_gemms", "fwd_barrier", "combine", "combine_bwd_router_wgrad", "bwd_barrier0", "bwd_gemms",
+              "fwd_gemm_gateup", "fwd_gemm_down", "fwd_barrier", "combine", "combine_bwd_router_wgrad", "bwd_barrier0", "bwd_gemms",
               "rs_sum_barrier", "unpermute", "grad_reduce_scatter_kernel", "step_total", "restore_start",
               "restore_ms"]
 
     def phase_ms(self):
         """Mean per-phase device times (needs FSEP_PHASE_TIMING=1 at layer creation), or None."""
-        out = (C.c_double * 19)()
-        if self.lib.mp_fsep_layer_phase_ms(self._h, out, 19) != 0:
+        out = (C.c_double * len(self.PHASES))()
+        if self.lib.mp_fsep_layer_phase_ms(self._h, out, len(self.PHASES)) != 0:
             return None
         return {k: round(out[i], 4) for i, k in enumerate(self.PHASES)}
 
