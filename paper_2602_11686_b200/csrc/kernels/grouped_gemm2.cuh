@@ -46,7 +46,8 @@ constexpr int EPI_STAGE_BYTES = EPI_WARPS * 32 * 32 * 4;
 // bf16 epilogues: per-warp [32 rows][64 B] row-piece transpose tile
 constexpr int EPI_STAGE16_BYTES = EPI_WARPS * 32 * 64;
 constexpr int smem_bytes(int epi) {
-  return epi == kEpiSwigluBwd ? 1024 + EPI_STAGE_OFF + EPI_STAGE_BYTES : 1024 + EPI_STAGE_OFF + EPI_STAGE16_BYTES;
+  return (epi == kEpiSwigluBwd || epi == kEpiBf16) ? 1024 + EPI_STAGE_OFF + EPI_STAGE_BYTES
+                                                   : 1024 + EPI_STAGE_OFF + EPI_STAGE16_BYTES;
 }
 static_assert(1024 + EPI_STAGE_OFF + EPI_STAGE_BYTES + (2 * MAX_GROUPS + 1) * 4 <= 232448,
               "SwiGLU-bwd staging + tile tables exceed shared memory");
@@ -83,6 +84,25 @@ __device__ __forceinline__ void warp_store_rows64(uint32_t stg, const uint4 (&v)
     const uint4 x = lds128(stg + 16 * (rr * 4 + (cg ^ ((rr >> 1) & 3))));
     auto* d = dst(rr);
     if (d != nullptr) reinterpret_cast<uint4*>(d)[cg] = x;
+  }
+  __syncwarp();
+}
+
+// Same for 128-B row pieces (64 bf16): 8 lanes per row, 4 rows per store
+// instruction; nval = valid 16-B pieces of each row (columns past N are not stored).
+template <typename Dst>
+__device__ __forceinline__ void warp_store_rows128(uint32_t stg, const uint4 (&v)[8], int nval, Dst dst) {
+  const int lane = static_cast<int>(threadIdx.x & 31);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) sts128(stg + 16 * (lane * 8 + (q ^ (lane & 7))), v[q]);
+  __syncwarp();
+  const int sub = lane >> 3, cg = lane & 7;
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int rr = it * 4 + sub;
+    const uint4 x = lds128(stg + 16 * (rr * 8 + (cg ^ (rr & 7))));
+    auto* d = dst(rr);
+    if (d != nullptr && cg < nval) reinterpret_cast<uint4*>(d)[cg] = x;
   }
   __syncwarp();
 }
@@ -320,9 +340,30 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
             }
           }
         } else if (kEpi == kEpiBf16) {
-          const uint32_t stg = ptx::smem_u32(smem + EPI_STAGE_OFF) + (warp - 2) * 2048;
           const long long row = p.group_off[g] + m_half + r;
           __nv_bfloat16* out = bf16_out_row(p, row);  // own row (row scatter resolved per lane)
+#ifndef FSEP_EPI_ROW64
+          // 64-column passes, 128-B row pieces (fewer, larger remote writes for the row scatter)
+          const uint32_t stg = ptx::smem_u32(smem + EPI_STAGE_OFF) + (warp - 2) * 4096;
+#pragma unroll 1
+          for (int j = 0; j < 2; ++j) {
+            const int c = half * 128 + j * 64;
+            const int col = nbk * BN + c;
+            if (col >= p.N) break;
+            float v[64];
+            tmem_ld32(taddr + c, *reinterpret_cast<float(*)[32]>(v));
+            if (col + 32 < p.N) tmem_ld32(taddr + c + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+            uint4 o[8];
+            pack_row64(v, *reinterpret_cast<uint4(*)[4]>(o));
+            pack_row64(v + 32, *reinterpret_cast<uint4(*)[4]>(o + 4));
+            warp_store_rows128(stg, o, min(8, (p.N - col) / 8), [&](int rr) {
+              __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(
+                  __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(out), rr));
+              return d == nullptr ? d : d + col;
+            });
+          }
+#else
+          const uint32_t stg = ptx::smem_u32(smem + EPI_STAGE_OFF) + (warp - 2) * 2048;
 #pragma unroll 1
           for (int j = 0; j < 4; ++j) {
             const int c = half * 128 + j * 32;
@@ -338,6 +379,7 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
               return d == nullptr ? d : d + col;
             });
           }
+#endif
         } else if (kEpi == kEpiSwigluFwd) {
           // tile columns [0,128) = gate f0.., [128,256) = up f0..; this warp: f in [64*half, 64*half+64)
           const uint32_t stg = ptx::smem_u32(smem + EPI_STAGE_OFF) + (warp - 2) * 2048;
