@@ -668,10 +668,13 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   if (ce_rs) {
     Rank& r = L.ranks[0];
     for (int q = 1; q < N; ++q) CK(cudaStreamWaitEvent(st, L.ev_ce[(r.rank + q) % N], 0));  // own pushes landed
-    barrier(L, st);  // ... and everyone else's
+    // ... and everyone else's: this barrier also orders every rank's dX GEMM (whose
+    // epilogue stored dX rows into our tok_rows) before the unpermute below
+    barrier(L, st);
     launch_grad_rs_sum(r.pt, r.grad_full, r.rs_stage, E, N, r.rank, L.S, L.flat, r.grad_shard, st);
+  } else {
+    barrier(L, st);
   }
-  barrier(L, st);
   mark(L, st, kPhBwdGemmBarrier);
   for (size_t v = 0; v < L.ranks.size(); ++v) {
     Rank& r = L.ranks[v];
