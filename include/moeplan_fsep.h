@@ -141,7 +141,8 @@ mp_status mp_fsep_layer_load_expert(mp_fsep_layer* layer, uint32_t expert, const
 mp_status mp_fsep_layer_load_router(mp_fsep_layer* layer, const void* wg, void* stream);
 
 /* Expert layout for the NEXT forward (host array E*N).  The shard restore for
- * it is issued on the layer's side stream at the next forward. */
+ * it is issued at the next forward (copy-engine pushes in real multi-GPU mode,
+ * a restore kernel on a side stream in virtual mode). */
 mp_status mp_fsep_layer_set_layout(mp_fsep_layer* layer, const uint8_t* A);
 
 /* Attach a planner (mp_fsep_planner_create): after every forward's router the
@@ -178,10 +179,14 @@ mp_status mp_fsep_layer_router_grad(mp_fsep_layer* layer, uint32_t vrank, float*
 /* Test/inspection export of a named internal buffer of rank `vrank` into dst
  * (device or host).  If dst is NULL only *needed is written.  Names:
  *   "topk_idx" i32[T][K], "topk_w" f32[T][K], "slot_dst" u32[T][K] (dst<<24|row),
- *   "R" u64[N][E], "S" u64[N][E][N], "seg_rows" i32[C], "seg_off" i32[C+1],
- *   "x_rows" bf16[rows][H], "y_rows" bf16[rows][H], "act" bf16[rows][F],
- *   "h" bf16[rows][2F] (interleaved gate/up 128-col blocks), "restored" bf16[C][3HF],
- *   "layout" u8[E][N], "status" u32[4] (device error flags)                     */
+ *   "dl" f32[T][K], "R" u64[N][E], "layout" u8[E][N], "seg_rows" i32[C],
+ *   "seg_off" i32[C], "slot_expert" i32[C], "total_rows" i32, "status" i32
+ *   (1 = receive-buffer overflow: segments dropped, step invalid),
+ *   "x_rows" / "dy_rows" bf16[cap][H], "row_src" i32[cap] (src<<26 | t*K+k, -1 pad),
+ *   "tok_rows" bf16[T*K][H] (this rank's slot rows: y after forward, dX after
+ *   backward), "h" bf16[cap][2F] (interleaved gate/up 128-col blocks),
+ *   "act" bf16[cap][F], "restored" bf16[C][3HF], "grad_full" f32[C][3HF],
+ *   "barrier_status" u32 (nonzero: a peer barrier timed out)                    */
 mp_status mp_fsep_layer_read(mp_fsep_layer* layer, const char* name, uint32_t vrank, void* dst, uint64_t bytes,
                              uint64_t* needed);
 
@@ -192,11 +197,12 @@ mp_status mp_fsep_layer_read(mp_fsep_layer* layer, const char* name, uint32_t vr
 mp_status mp_fsep_layer_stats(mp_fsep_layer* layer, uint64_t* kernel_launches, double* gemm_ms, double* gemm_flops);
 mp_status mp_fsep_layer_stats_reset(mp_fsep_layer* layer);
 /* Per-phase mean times (ms) since the last reset, when the layer was created with
- * FSEP_PHASE_TIMING=1 in the environment.  out[0..15]: consecutive main-stream
- * phases (param barrier, router+scan, R barrier, plan, dispatch, dispatch barrier,
- * restore wait, fwd GEMMs, barrier, combine, combine-bwd + router wgrad, barrier,
- * bwd GEMMs, barrier, unpermute, grad reduce-scatter); out[16] whole step;
- * out[17] restore start offset; out[18] restore duration.  n >= 19. */
+ * FSEP_PHASE_TIMING=1 in the environment.  out[0..16]: consecutive main-stream
+ * phases (param barrier, router+scan, R barrier, plan, dispatch, dispatch barrier
+ * (+ expansion), restore wait, gate-up GEMM, down GEMM, barrier, combine,
+ * combine-bwd + router wgrad, barrier (+ expansion), bwd GEMMs, reduce-scatter
+ * wait + barrier + sum, unpermute, SM grad reduce-scatter); out[17] whole step;
+ * out[18] restore start offset; out[19] restore issue-to-join time.  n >= 20. */
 mp_status mp_fsep_layer_phase_ms(mp_fsep_layer* layer, double* out, uint32_t n);
 
 /* Capture forward+backward into a CUDA graph and replay it (bench path). */
