@@ -153,7 +153,7 @@ mp_status mp_fsep_layer_set_layout(mp_fsep_layer* layer, const uint8_t* A);
  * layer or be detached first. */
 mp_status mp_fsep_layer_attach_planner(mp_fsep_layer* layer, mp_fsep_planner* planner);
 
-/* Layer chaining (PAPER Fig.5 schedule): after `layer`'s dispatch in each forward,
+/* Layer chaining (PAPER Fig.5 schedule): after `layer`'s gate-up GEMM in each forward,
  * the shard restore of `next` (the next MoE layer, same devices) is issued on
  * next's copy engines, so it overlaps `layer`'s expert MLP; next's forward then
  * skips its own restore.  Copy-engine mode (real multi-GPU) only; NULL unchains.

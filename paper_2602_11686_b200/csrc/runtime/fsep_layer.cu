@@ -516,15 +516,6 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
                     st);
   mark(L, st, kPhDispatch);
   if (restore && ce && !prefetched && L.restore_split) push_restore(L, st, 1, kMaxExperts);
-  // Fig.5 schedule: the next layer's expert restore travels on the copy engines
-  // while this layer's expert MLP runs (safe: every rank has passed this step's
-  // parameter barrier, so all of the previous step's work is complete).
-  if (L.next && L.next->ce_mode && !L.next->prefetched && (!L.next->resident || L.next->restore_dirty)) {
-    Layer& nx = *L.next;
-    snapshot_layout(nx, st);
-    push_restore(nx, st);
-    nx.prefetched = true;
-  }
   barrier(L, st);
   if (L.dedupe)  // token rows that crossed NVLink once per device -> this rank's slot rows
     for (Rank& r : L.ranks)
@@ -548,7 +539,21 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
     g.out2 = r.act;
     g.ldo2 = F;
     gemm(L, GemmKind::kFwdGateUp, r.tm_x_k, r.tm_w13_k, r.tm_w13_k128, g, st);
-    if (&r == &L.ranks.back()) mark(L, st, kPhFwdGateUp);
+    if (&r == &L.ranks.back()) {
+      mark(L, st, kPhFwdGateUp);
+      // Fig.5 schedule: the next layer's expert restore travels on the copy engines
+      // while this layer's down GEMM, combine and the next layer's router/dispatch
+      // run.  Issued after the gate-up GEMM, which has waited for all of this
+      // layer's restored slots, so the two restores never share the copy engines
+      // (safe: every rank has passed this step's parameter barrier, so all of the
+      // previous step's work is complete).
+      if (L.next && L.next->ce_mode && !L.next->prefetched && (!L.next->resident || L.next->restore_dirty)) {
+        Layer& nx = *L.next;
+        snapshot_layout(nx, st);
+        push_restore(nx, st);
+        nx.prefetched = true;
+      }
+    }
     GroupedGemmArgs g2 = g;
     g2.N = H;
     g2.K = F;
