@@ -378,7 +378,7 @@ def main():
         rows = int(layers[0].read("total_rows").view(np.int32)[0])
         dist.all_gather_object(allp, {"phases": phases, "gemm_ms": sum(s_["gemm_ms"] for s_ in sts), "rows": rows})
         keys = ["router_scan", "dispatch", "fwd_gemm_gateup", "fwd_gemm_down", "fwd_gemms", "fwd_barrier", "combine_bwd_router_wgrad", "bwd_gemms",
-                "rs_sum_barrier", "step_total"]
+                "rs_push_wait", "rs_barrier", "rs_sum", "step_total"]
         per_rank = {k: [round(a["phases"].get(k, 0.0), 3) for a in allp] for k in keys}
         per_rank["gemm_ms"] = [round(a["gemm_ms"], 3) for a in allp]
         per_rank["recv_rows_last_step"] = [a["rows"] for a in allp]

@@ -197,12 +197,13 @@ mp_status mp_fsep_layer_read(mp_fsep_layer* layer, const char* name, uint32_t vr
 mp_status mp_fsep_layer_stats(mp_fsep_layer* layer, uint64_t* kernel_launches, double* gemm_ms, double* gemm_flops);
 mp_status mp_fsep_layer_stats_reset(mp_fsep_layer* layer);
 /* Per-phase mean times (ms) since the last reset, when the layer was created with
- * FSEP_PHASE_TIMING=1 in the environment.  out[0..16]: consecutive main-stream
+ * FSEP_PHASE_TIMING=1 in the environment.  out[0..18]: consecutive main-stream
  * phases (param barrier, router+scan, R barrier, plan, dispatch, dispatch barrier
  * (+ expansion), restore wait, gate-up GEMM, down GEMM, barrier, combine,
- * combine-bwd + router wgrad, barrier (+ expansion), bwd GEMMs, reduce-scatter
- * wait + barrier + sum, unpermute, SM grad reduce-scatter); out[17] whole step;
- * out[18] restore start offset; out[19] restore issue-to-join time.  n >= 20. */
+ * combine-bwd + router wgrad, barrier (+ expansion), bwd GEMMs, wait for own
+ * reduce-scatter pushes, barrier, reduce-scatter sum, unpermute, SM grad
+ * reduce-scatter); out[19] whole step; out[20] restore start offset; out[21]
+ * restore issue-to-join time.  n >= 22. */
 mp_status mp_fsep_layer_phase_ms(mp_fsep_layer* layer, double* out, uint32_t n);
 
 /* Capture forward+backward into a CUDA graph and replay it (bench path). */

@@ -17,9 +17,10 @@
 //             down GEMM's epilogue stores y rows into the token owners' slot rows)
 //             == barrier ==  combine (local slot rows, gate-weighted fp32 sum)
 //   backward  combine bwd (dw, dl; dY rows -> expert devices) + router wgrad GEMM
-//             == barrier ==  dgrad (SwiGLU'), wgrad dW2 -> push W2 grad chunks to their
-//             owners (copy engines) under the dW13 wgrad -> push W13 chunks under the
-//             dX GEMM (its epilogue stores dX rows into the owners' slot rows)
+//             == barrier ==  dgrad (SwiGLU'), wgrad dW13 -> push W13 grad chunks to
+//             their owners (copy engines) under the dW2 wgrad and the dX GEMM ->
+//             push W2 chunks under the dX GEMM (its epilogue stores dX rows into the
+//             owners' slot rows)
 //             == barrier ==  owner-side reduce-scatter sum, unpermute bwd (+ router dx)
 // Only the copy-engine path needs the layout on the host: the forward waits on
 // the previous step's planner callback (which ran right after that step's
@@ -187,6 +188,8 @@ enum Phase : int {
   kPhCombineBwd,
   kPhCombineBwdBarrier,
   kPhBwdGemm,
+  kPhRsPushWait,  // own reduce-scatter pushes landed (copy-engine mode)
+  kPhRsBarrier,   // everyone's pushes landed
   kPhBwdGemmBarrier,
   kPhUnpermute,
   kPhGradRS,
@@ -600,8 +603,7 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   mark(L, st, kPhCombineBwdBarrier);
   CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][2], st));
   // Weight gradients first: in copy-engine mode their reduce-scatter pushes run
-  // on the copy engines underneath the GEMMs that follow (W2 part under dW13,
-  // W13 part under dX).
+  // on the copy engines underneath the GEMMs that follow.
   const bool rs = N > 1 && !L.resident;  // pure EP: gradients stay whole on their single host
   const bool ce_rs = L.ce_mode && rs;
   // Push this rank's replica-gradient chunks [lo, hi) of the flat vector to their
@@ -623,6 +625,9 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
     }
   };
   const long long w2_lo = 2LL * F * H;
+  // Order: dH (SwiGLU' fused), dW13, dW2, dX.  The W13 part of the replica
+  // gradient chunks (2/3 of the reduce-scatter bytes) is pushed as soon as dW13 is
+  // done and travels under dW2 + dX; the W2 part travels under dX.
   for (Rank& r : L.ranks) {
     GroupedGemmArgs g = gemm_args(L, r);  // dAct -> dH (SwiGLU backward fused)
     g.N = F;
@@ -632,19 +637,6 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
     g.aux = r.h;
     g.ld_aux = 2 * F;
     gemm(L, GemmKind::kBwdDownDgrad, r.tm_dy_k, r.tm_w2_mn, r.tm_w2_mn, g, st);
-    GroupedGemmArgs g3 = gemm_args(L, r);  // dW2 = dY^T act
-    g3.M = H;
-    g3.N = F;
-    g3.out = r.grad_full + 2LL * F * H;
-    g3.ldo = F;
-    g3.out_group_stride = L.flat;
-    gemm(L, GemmKind::kBwdWgrad, r.tm_dy_mn, r.tm_act_mn, r.tm_act_mn, g3, st);
-  }
-  if (ce_rs) {  // W2 part of the gradient chunks travels under the dW13 GEMM
-    CK(cudaEventRecord(L.ev_w2, st));
-    push_grads(L.ev_w2, w2_lo, L.flat);
-  }
-  for (Rank& r : L.ranks) {
     GroupedGemmArgs g4 = gemm_args(L, r);  // dW13 = dH^T X
     g4.M = 2 * F;
     g4.N = H;
@@ -653,9 +645,22 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
     g4.out_group_stride = L.flat;
     gemm(L, GemmKind::kBwdWgrad, r.tm_dh_mn, r.tm_x_mn, r.tm_x_mn, g4, st);
   }
-  if (ce_rs) {  // W13 part under the dX GEMM
+  if (ce_rs) {
     CK(cudaEventRecord(L.ev_wg, st));
     push_grads(L.ev_wg, 0, w2_lo);
+  }
+  for (Rank& r : L.ranks) {
+    GroupedGemmArgs g3 = gemm_args(L, r);  // dW2 = dY^T act
+    g3.M = H;
+    g3.N = F;
+    g3.out = r.grad_full + 2LL * F * H;
+    g3.ldo = F;
+    g3.out_group_stride = L.flat;
+    gemm(L, GemmKind::kBwdWgrad, r.tm_dy_mn, r.tm_act_mn, r.tm_act_mn, g3, st);
+  }
+  if (ce_rs) {
+    CK(cudaEventRecord(L.ev_w2, st));
+    push_grads(L.ev_w2, w2_lo, L.flat);
   }
   for (Rank& r : L.ranks) {
     GroupedGemmArgs g2 = gemm_args(L, r);  // dX rows
@@ -673,12 +678,16 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   if (ce_rs) {
     Rank& r = L.ranks[0];
     for (int q = 1; q < N; ++q) CK(cudaStreamWaitEvent(st, L.ev_ce[(r.rank + q) % N], 0));  // own pushes landed
+    mark(L, st, kPhRsPushWait);
     // ... and everyone else's: this barrier also orders every rank's dX GEMM (whose
     // epilogue stored dX rows into our tok_rows) before the unpermute below
     barrier(L, st);
+    mark(L, st, kPhRsBarrier);
     launch_grad_rs_sum(r.pt, r.grad_full, r.rs_stage, E, N, r.rank, L.S, L.flat, r.grad_shard, st);
   } else {
+    mark(L, st, kPhRsPushWait);
     barrier(L, st);
+    mark(L, st, kPhRsBarrier);
   }
   mark(L, st, kPhBwdGemmBarrier);
   for (size_t v = 0; v < L.ranks.size(); ++v) {
