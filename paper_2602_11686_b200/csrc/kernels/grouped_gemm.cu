@@ -133,6 +133,11 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
     return v && std::string(v) == "0";
   }();
   if (no_tail) p.policy |= 0x100;
+  static const bool rr_sched = [] {  // FSEP_GEMM_SCHED=rr: plain round robin, groups in index order
+    const char* v = std::getenv("FSEP_GEMM_SCHED");
+    return v && std::string(v) == "rr";
+  }();
+  if (rr_sched) p.policy |= 0x200;
   switch (kind) {
     case GemmKind::kFwdGateUp: launch_pair<false, false, false, kEpiSwigluFwd>(tmA, tmB, p, num_sms, stream); break;
     case GemmKind::kFwdDown: launch_pair<false, false, false, kEpiBf16>(tmA, tmB, p, num_sms, stream); break;

@@ -130,7 +130,10 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   __shared__ int tile_start[MAX_GROUPS + 1];  // first tile of each group (static smem: LDS, not generic loads)
-  __shared__ int group_mbs[MAX_GROUPS];       // M tiles per group
+  // M-grouped: M tiles of each group.  K-grouped (every group has p.M / BM M tiles):
+  // the group at each schedule position.
+  __shared__ int group_mbs[MAX_GROUPS];
+  int* group_id = group_mbs;
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -141,12 +144,33 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
   const int cluster = blockIdx.x >> 1;
   const int nclusters = gridDim.x >> 1;
 
+  // Schedule order of the groups.  K-grouped (wgrad): descending row count (ties:
+  // lower index first), so that with the snake assignment below the tiles go out
+  // longest-first -- the per-tile cost is the group's row count, which is very
+  // skewed under Zipf routing (a static round robin left some CTA pairs with
+  // ~20% more work than the mean).  M-grouped: identity (equal-cost tiles, and the
+  // restored slots become ready in slot order).
+  if (kGroupK) {
+    for (int i = static_cast<int>(threadIdx.x); i < G; i += static_cast<int>(blockDim.x)) {
+      int pos = i;
+      if (!(p.policy & 0x200)) {
+        const int ri = p.group_rows[i];
+        pos = 0;
+        for (int j = 0; j < G; ++j) {
+          const int rj = p.group_rows[j];
+          pos += (rj > ri || (rj == ri && j < i)) ? 1 : 0;
+        }
+      }
+      group_id[pos] = i;
+    }
+    __syncthreads();
+  }
+  auto gid = [&](int gi) { return kGroupK ? group_id[gi] : gi; };
   if (threadIdx.x == 0) {
     int acc = 0;
-    for (int g = 0; g < G; ++g) {
-      tile_start[g] = acc;
-      group_mbs[g] = kGroupK ? p.M / BM : (p.group_rows[g] + BM - 1) / BM;
-      acc += group_mbs[g] * nb;
+    for (int gi = 0; gi < G; ++gi) {
+      tile_start[gi] = acc;
+      acc += (kGroupK ? p.M / BM : (group_mbs[gi] = (p.group_rows[gi] + BM - 1) / BM)) * nb;
     }
     tile_start[G] = acc;
     for (int s = 0; s < STAGES; ++s) {
@@ -174,12 +198,20 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
   auto decode = [&](int t, int& g, int& mb, int& nbk) {
     // every role walks its tiles in increasing order: resume the group search
     while (tile_start[gdec + 1] <= t) ++gdec;
-    g = gdec;
-    const int local = t - tile_start[g];
-    const int mbs = group_mbs[g];
+    g = gid(gdec);
+    const int local = t - tile_start[gdec];
+    const int mbs = kGroupK ? p.M / BM : group_mbs[gdec];
     raster_tile(local, mbs, nb, p.raster == 0 ? 16 : p.raster, kGroupK, mb, nbk);  // default: 16-tile m-chunks
   };
   auto k_blocks = [&](int g) { return kGroupK ? p.group_rows[g] / BK : p.K / BK; };
+  // Tile of this CTA pair in wave w.  K-grouped: snake order (even waves ascending,
+  // odd waves descending over the pairs), so consecutive waves hand the costlier
+  // tiles of the descending-cost list to alternate ends -- LPT-like balance.
+  // M-grouped: plain round robin (equal-cost tiles; the snake measured 4% slower
+  // there).  Tile indices increase with w for every pair (the group search relies on it).
+  auto wave_tile = [&](int w) {
+    return w * nclusters + ((kGroupK && (w & 1) && !(p.policy & 0x200)) ? nclusters - 1 - cluster : cluster);
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer (both CTAs)
@@ -190,7 +222,7 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       int ready_g = -1;
-      for (int t = cluster; t < total_tiles; t += nclusters) {
+      for (int w = 0, t = wave_tile(0); t < total_tiles; t = wave_tile(++w)) {
         int g, mb, nbk;
         decode(t, g, mb, nbk);
         const int nk = k_blocks(g);
@@ -244,7 +276,7 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
-      for (int t = cluster; t < total_tiles; t += nclusters, ++it) {
+      for (int w = 0, t = wave_tile(0); t < total_tiles; t = wave_tile(++w), ++it) {
         int g, mb, nbk;
         decode(t, g, mb, nbk);
         const int nk = k_blocks(g);
@@ -285,7 +317,7 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
     const int half0 = NHALF == 1 ? static_cast<int>(warp - 2) >> 2 : 0;
     const int r = static_cast<int>(quarter * 32 + lane);  // row within this CTA's 128 rows
     int it = 0;
-    for (int t = cluster; t < total_tiles; t += nclusters, ++it) {
+    for (int w = 0, t = wave_tile(0); t < total_tiles; t = wave_tile(++w), ++it) {
       int g, mb, nbk;
       decode(t, g, mb, nbk);
       const int as = it & 1;
