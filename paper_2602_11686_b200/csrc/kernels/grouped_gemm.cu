@@ -138,6 +138,11 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
     return v && std::string(v) == "rr";
   }();
   if (rr_sched) p.policy |= 0x200;
+  static const bool rel_cluster = [] {  // FSEP_TMEM_RELEASE=cluster: cluster-scope release on the TMEM hand-off
+    const char* v = std::getenv("FSEP_TMEM_RELEASE");
+    return v && std::string(v) == "cluster";
+  }();
+  if (rel_cluster) p.policy |= 0x400;
   switch (kind) {
     case GemmKind::kFwdGateUp: launch_pair<false, false, false, kEpiSwigluFwd>(tmA, tmB, p, num_sms, stream); break;
     case GemmKind::kFwdDown: launch_pair<false, false, false, kEpiBf16>(tmA, tmB, p, num_sms, stream); break;

@@ -49,6 +49,7 @@ struct GemmParams {
   int policy;  // L2 hints: bits 0-1 A, bits 2-3 B (0 default for the mode, 1 normal, 2 evict_first, 3 evict_last);
                // bit 8: pair kernel runs a <=128-column last N tile at full N=256 (no N=128 tail MMA)
                // bit 9: pair kernel uses a plain round-robin tile schedule (no snake / LPT group order)
+               // bit 10: pair kernel releases the TMEM accumulator with a cluster-scope release (A/B)
   int raster;  // tile order within a group: 0 mode default, 1 m-inner, 2 n-inner, 3+ = m-chunks of `raster` tiles, n-inner
   // Optional per-group readiness (M-grouped only): before loading B of group g the
   // producer waits until ready[g * ready_n + q] has reached ready_epoch for all

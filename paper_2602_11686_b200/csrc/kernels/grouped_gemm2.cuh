@@ -512,7 +512,12 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(&tempty_bar[as], 0);
+      if (lane == 0) {
+        if (p.policy & 0x400)
+          mbar_arrive_cluster(&tempty_bar[as], 0);  // FSEP_TMEM_RELEASE=cluster (A/B)
+        else
+          mbar_arrive_remote(&tempty_bar[as], 0);
+      }
     }
   }
   __syncthreads();

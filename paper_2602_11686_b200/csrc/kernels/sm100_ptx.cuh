@@ -176,6 +176,16 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta)
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
+// Remote arrive with the default semantics (.release at .cta scope).  Enough for the
+// TMEM-accumulator hand-off: the tcgen05.ld's are ordered before it by
+// tcgen05.fence::before_thread_sync, and the epilogue's global stores need no
+// ordering against the next MMAs.  The .cluster-scope release above makes the
+// warp wait (ERRBAR) until all of its outstanding global stores are performed.
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
 // Peer-bit cleared: the complete_tx of both CTAs of the pair lands on CTA 0's barrier.
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
 __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t c0, int32_t c1,
