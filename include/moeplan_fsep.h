@@ -203,7 +203,9 @@ mp_status mp_fsep_layer_stats_reset(mp_fsep_layer* layer);
  * combine-bwd + router wgrad, barrier (+ expansion), bwd GEMMs, wait for own
  * reduce-scatter pushes, barrier, reduce-scatter sum, unpermute, SM grad
  * reduce-scatter); out[19] whole step; out[20] restore start offset; out[21]
- * restore issue-to-join time.  n >= 22. */
+ * restore issue-to-join time; out[22] forward top -> first phase (layout
+ * snapshot + H2D); out[23] idle gap between the previous step's end and this
+ * step's top; out[24] host time blocked on the planner per step.  n >= 23. */
 mp_status mp_fsep_layer_phase_ms(mp_fsep_layer* layer, double* out, uint32_t n);
 
 /* Capture forward+backward into a CUDA graph and replay it (bench path). */

@@ -7,6 +7,7 @@
 //    replica split reproduces lite_routing (planner.cpp:277-282);
 //  * every token-slot's destination (device, row) and the per-device segment
 //    layout are integer functions of R, the layout and the ranks.
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 #include <cuda_bf16.h>
@@ -611,16 +612,40 @@ __global__ void grad_rs_sum_kernel(const PlanTables* __restrict__ pt, const floa
   }
   float4* dst = reinterpret_cast<float4*>(grad_shard + static_cast<long long>(e) * S);
   const long long n = S / 4;
-  for (long long i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    float4 a = src[0][i];
+  // 4 float4 per thread per source in flight (streaming loads / stores: nothing
+  // here is re-read), summed in ascending host order
+  constexpr int U = 4;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < n; i += U * stride) {
+    float4 a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) a[u] = __ldcs(src[0] + i + u * stride);
     for (int h = 1; h < nh; ++h) {
-      const float4 b = src[h][i];
+      float4 b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) b[u] = __ldcs(src[h] + i + u * stride);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        a[u].x += b[u].x;
+        a[u].y += b[u].y;
+        a[u].z += b[u].z;
+        a[u].w += b[u].w;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) __stcs(dst + i + u * stride, a[u]);
+  }
+  for (; i < n; i += stride) {
+    float4 a = __ldcs(src[0] + i);
+    for (int h = 1; h < nh; ++h) {
+      const float4 b = __ldcs(src[h] + i);
       a.x += b.x;
       a.y += b.y;
       a.z += b.z;
       a.w += b.w;
     }
-    dst[i] = a;
+    __stcs(dst + i, a);
   }
 }
 
@@ -814,7 +839,7 @@ void launch_unpack_grad(const float* chunk, long long lo, long long hi, int H, i
 namespace fsep {
 void launch_grad_rs_sum(const PlanTables* pt, const float* grad_full, const float* stage, int E, int N, int rank,
                         long long S, long long flat, float* grad_shard, cudaStream_t st) {
-  grad_rs_sum_kernel<<<dim3(128, E), 256, 0, st>>>(pt, grad_full, stage, N, rank, S, flat, grad_shard);
+  grad_rs_sum_kernel<<<dim3(std::max(1, 2 * 148 * 8 / E), E), 256, 0, st>>>(pt, grad_full, stage, N, rank, S, flat, grad_shard);
   count_launch();
 }
 }  // namespace fsep

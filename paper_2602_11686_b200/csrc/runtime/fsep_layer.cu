@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <array>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -169,6 +170,7 @@ extern "C" struct mp_fsep_layer {
   static constexpr int kPhaseRing = 64;
   bool phase_on = false;
   std::vector<std::array<cudaEvent_t, 24>> ev_p;
+  double host_wait_ms = 0.0;  // host time blocked on the previous step's planner (since reset)
 };
 
 namespace {
@@ -195,6 +197,7 @@ enum Phase : int {
   kPhGradRS,
   kPhRestoreBegin,  // side stream
   kPhRestoreEnd,
+  kPhStepBegin,  // top of the forward, before the layout snapshot / H2D
   kPhCount
 };
 
@@ -403,7 +406,11 @@ GroupedGemmArgs gemm_args(Layer& L, Rank& r) {
 // previous step's planner callback) and ship it to the device on `st`.
 void snapshot_layout(Layer& L, cudaStream_t st) {
   const int E = L.E, N = L.N;
-  if (L.planner_pending) CK(cudaEventSynchronize(L.ev_planned));
+  if (L.planner_pending) {
+    const auto t0 = std::chrono::steady_clock::now();
+    CK(cudaEventSynchronize(L.ev_planned));
+    L.host_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
   uint8_t* snap = L.layout_ring + (L.step_no % 4) * static_cast<size_t>(E) * N;
   std::memcpy(snap, L.layout_host, static_cast<size_t>(E) * N);
   L.cur_layout = snap;
@@ -443,6 +450,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   if (T < 0 || T > L.T_max) throw Error(ErrorKind::invalid_argument, "forward: n_tokens exceeds max_tokens");
   const int E = L.E, K = L.K, H = L.H, F = L.F, N = L.N, C = L.C;
   L.T_step = T;
+  mark(L, st, kPhStepBegin);
   const long long TH = static_cast<long long>(T) * H;
   // 1. layout for this step (planner result of the previous step, or set_layout)
   const bool ce = L.ce_mode;
@@ -1164,7 +1172,24 @@ mp_status mp_fsep_layer_phase_ms(mp_fsep_layer* L, double* out, uint32_t n) {
       }
       cudaGetLastError();
     }
+    // out[kPhStepBegin]: top of the forward -> first phase mark (layout snapshot / H2D);
+    // out[kPhCount]: previous step's end -> this step's top (idle gap between steps);
+    // out[kPhCount + 1]: host time blocked on the planner per step
+    double gap = 0.0;
+    long long ngap = 0;
+    for (long long s = L->step_no - cnt; s < L->step_no; ++s) {
+      auto& ev = L->ev_p[static_cast<size_t>(s % mp_fsep_layer::kPhaseRing)];
+      float a = 0.f;
+      if (cudaEventElapsedTime(&a, ev[kPhStepBegin], ev[kPhFwdBegin]) == cudaSuccess) acc[kPhStepBegin] += a;
+      if (s > L->stats_from) {
+        auto& pv = L->ev_p[static_cast<size_t>((s - 1) % mp_fsep_layer::kPhaseRing)];
+        if (cudaEventElapsedTime(&a, pv[kPhGradRS], ev[kPhStepBegin]) == cudaSuccess) gap += a, ++ngap;
+      }
+      cudaGetLastError();
+    }
     for (int i = 0; i < kPhCount; ++i) out[i] = acc[static_cast<size_t>(i)] / static_cast<double>(cnt);
+    if (n > static_cast<uint32_t>(kPhCount)) out[kPhCount] = ngap ? gap / static_cast<double>(ngap) : 0.0;
+    if (n > static_cast<uint32_t>(kPhCount) + 1) out[kPhCount + 1] = L->host_wait_ms / static_cast<double>(cnt);
   });
 }
 
@@ -1172,6 +1197,7 @@ mp_status mp_fsep_layer_stats_reset(mp_fsep_layer* L) {
   return guarded([&] {
     require(L, "mp_fsep_layer_stats_reset: NULL layer");
     L->stats_from = L->step_no;
+    L->host_wait_ms = 0.0;
   });
 }
 
