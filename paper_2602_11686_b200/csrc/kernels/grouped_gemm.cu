@@ -127,7 +127,18 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
   GemmParams p{a.num_groups, a.group_rows, a.group_off, a.M,    a.N,    a.K,   a.out,
                a.ldo,        a.out_group_stride, a.out2,    a.ldo2, a.aux, a.ld_aux, a.policy, a.raster,
                a.ready,      a.ready_epoch,      a.ready_n,
-               a.row_src,    a.scatter,          a.scatter_rows};
+               a.row_src,    a.scatter,          a.scatter_rows, nullptr};
+  static const bool wave_sync = [] {  // FSEP_WAVE_SYNC=0: free-running producers
+    const char* v = std::getenv("FSEP_WAVE_SYNC");
+    return !(v && std::string(v) == "0");
+  }();
+  // long-K M-grouped GEMMs only: their A / B panels (256 x K) do not stay in L2 when the
+  // CTA pairs drift apart along K (Mixtral up-dgrad, K = 28672: DRAM reads 11.9 -> 9.7 GB,
+  // step +2.5-5%); short-K panels fit in L2 anyway and the barrier only costs (fine config)
+  if (wave_sync && a.wave_sync != nullptr && kind != GemmKind::kBwdWgrad && a.K >= 4096) {
+    cudaMemsetAsync(a.wave_sync, 0, kWaveSyncMax * sizeof(int), stream);
+    p.wave_sync = a.wave_sync;
+  }
   static const bool no_tail = [] {
     const char* v = std::getenv("FSEP_GEMM_NTAIL");
     return v && std::string(v) == "0";
@@ -159,7 +170,7 @@ void launch_grouped_gemm(GemmKind kind, const CUtensorMap& tmA, const CUtensorMa
   GemmParams p{a.num_groups, a.group_rows, a.group_off, a.M,    a.N,    a.K,   a.out,
                a.ldo,        a.out_group_stride, a.out2,    a.ldo2, a.aux, a.ld_aux, a.policy, a.raster,
                a.ready,      a.ready_epoch,      a.ready_n,
-               a.row_src,    a.scatter,          a.scatter_rows};
+               a.row_src,    a.scatter,          a.scatter_rows, nullptr};
   switch (kind) {
     case GemmKind::kFwdGateUp: launch_one<false, false, false, kEpiSwigluFwd>(tmA, tmB, p, num_sms, stream); break;
     case GemmKind::kFwdDown: launch_one<false, false, false, kEpiBf16>(tmA, tmB, p, num_sms, stream); break;

@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include "kernels/fsep_types.cuh"
 #include "kernels/sm100_ptx.cuh"
 
 namespace fsep {
@@ -64,6 +65,12 @@ struct GemmParams {
   const int* row_src;
   __nv_bfloat16* const* scatter;
   long long scatter_rows;
+  // Optional wave synchronisation (pair kernel, M-grouped): before loading the tiles
+  // of wave w every CTA's producer waits (bounded) until all CTAs with a tile in
+  // wave w have issued the loads of wave w-1, so the CTAs stream the shared A / B
+  // panels along K in step and the panels are fetched from DRAM once per wave.
+  // wave_sync[w] are arrival counters, zeroed before the launch.
+  int* wave_sync;
 };
 
 __device__ __forceinline__ __nv_bfloat16* bf16_out_row(const GemmParams& p, long long row) {
@@ -88,6 +95,16 @@ __device__ __forceinline__ void wait_group_ready(const GemmParams& p, int g) {
   }
   // the chunks were written by copy engines (generic proxy); TMA reads via the async proxy
   asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ void wave_barrier(int* ctr, int expected) {
+  atomicAdd(ctr, 1);
+  for (int spin = 0; spin < 4000; ++spin) {  // bounded (~0.4 ms): never a hang if CTAs are not co-resident
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    if (v >= expected) break;
+    __nanosleep(64);
+  }
 }
 
 namespace gemm {

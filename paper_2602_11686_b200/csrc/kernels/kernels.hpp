@@ -38,6 +38,7 @@ struct GroupedGemmArgs {
   const int* row_src = nullptr;  // optional row scatter of the bf16 epilogue (see GemmParams)
   __nv_bfloat16* const* scatter = nullptr;
   long long scatter_rows = 0;
+  int* wave_sync = nullptr;  // optional wave-synchronisation counters (see GemmParams), zeroed by the launcher
 };
 
 enum class GemmKind : int {

@@ -98,6 +98,7 @@ struct Rank {
   uint32_t* slot_dst = nullptr;
   uint8_t* layout_dev = nullptr;
   PlanTables* pt = nullptr;
+  int* wave_sync = nullptr;  // grouped-GEMM wave-synchronisation counters (FSEP_WAVE_SYNC=1)
   CUtensorMap tm_w13_k128{}, tm_w2_k128{};  // K-major weight maps with 128-row boxes (CTA-pair kernel)
   CUtensorMap tm_x_k{}, tm_w13_k{}, tm_act_k{}, tm_w2_k{}, tm_dy_k{}, tm_w2_mn{}, tm_dh_k{}, tm_w13_mn{}, tm_dy_mn{},
       tm_act_mn{}, tm_dh_mn{}, tm_x_mn{};
@@ -322,6 +323,7 @@ void allocate_rank(Layer& L, Rank& r) {
   accp(nblk * E * 4 * 2);  // blk_hist, blk_base
   accp(E * N);            // layout
   accp(sizeof(PlanTables));
+  accp(kWaveSyncMax * sizeof(int));
   CK(cudaMalloc(&r.priv, align_up(b, 2 << 20)));
   CK(cudaMemset(r.priv, 0, align_up(b, 2 << 20)));
   Carver cp{static_cast<char*>(r.priv)};
@@ -350,6 +352,7 @@ void allocate_rank(Layer& L, Rank& r) {
   r.blk_base = cp.take<int>(nblk * E);
   r.layout_dev = cp.take<uint8_t>(E * N);
   r.pt = cp.take<PlanTables>(1);
+  r.wave_sync = cp.take<int>(kWaveSyncMax);
   build_maps(L, r);
 }
 
@@ -399,6 +402,7 @@ GroupedGemmArgs gemm_args(Layer& L, Rank& r) {
   g.num_groups = L.C;
   g.group_rows = r.pt->seg_rows_pad;
   g.group_off = r.pt->seg_off;
+  g.wave_sync = r.wave_sync;
   return g;
 }
 
