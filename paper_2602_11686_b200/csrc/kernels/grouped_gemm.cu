@@ -135,7 +135,16 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
   // long-K M-grouped GEMMs only: their A / B panels (256 x K) do not stay in L2 when the
   // CTA pairs drift apart along K (Mixtral up-dgrad, K = 28672: DRAM reads 11.9 -> 9.7 GB,
   // step +2.5-5%); short-K panels fit in L2 anyway and the barrier only costs (fine config)
-  if (wave_sync && a.wave_sync != nullptr && kind != GemmKind::kBwdWgrad && a.K >= 4096) {
+  // K-grouped wgrad: only when every group spans several waves (equal-cost tiles within a
+  // wave; a wave that mixes groups of different row counts would idle at the barrier)
+  static const bool wave_sync_wgrad = [] {  // FSEP_WAVE_SYNC_WGRAD=0: wgrad producers free-running
+    const char* v = std::getenv("FSEP_WAVE_SYNC_WGRAD");
+    return !(v && std::string(v) == "0");
+  }();
+  const bool long_k = kind == GemmKind::kBwdWgrad
+                          ? wave_sync_wgrad && (a.M / gemm2::BM) * ((a.N + gemm2::BN - 1) / gemm2::BN) >= 2 * num_sms
+                          : a.K >= 4096;
+  if (wave_sync && a.wave_sync != nullptr && long_k) {
     cudaMemsetAsync(a.wave_sync, 0, kWaveSyncMax * sizeof(int), stream);
     p.wave_sync = a.wave_sync;
   }
