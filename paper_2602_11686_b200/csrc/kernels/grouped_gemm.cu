@@ -144,6 +144,14 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
   const bool long_k = kind == GemmKind::kBwdWgrad
                           ? wave_sync_wgrad && (a.M / gemm2::BM) * ((a.N + gemm2::BN - 1) / gemm2::BN) >= 2 * num_sms
                           : a.K >= 4096;
+  // FSEP_WGRAD_RASTER: tile order of the wgrad launches (A/B; see GemmParams::raster).  n-inner
+  // for the Mixtral dW13 (112 x 16 tiles) halves its DRAM reads (10.8 -> 5.8 GB) but measured
+  // ~1% slower over the step, so the default stays 16-tile m-chunks.
+  static const int wgrad_raster = [] {
+    const char* v = std::getenv("FSEP_WGRAD_RASTER");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (kind == GemmKind::kBwdWgrad && p.raster == 0) p.raster = wgrad_raster;
   if (wave_sync && a.wave_sync != nullptr && long_k) {
     cudaMemsetAsync(a.wave_sync, 0, kWaveSyncMax * sizeof(int), stream);
     p.wave_sync = a.wave_sync;
