@@ -170,7 +170,7 @@ extern "C" struct mp_fsep_layer {
   // optional per-phase event timing (FSEP_PHASE_TIMING=1)
   static constexpr int kPhaseRing = 64;
   bool phase_on = false;
-  std::vector<std::array<cudaEvent_t, 24>> ev_p;
+  std::vector<std::array<cudaEvent_t, 26>> ev_p;
   double host_wait_ms = 0.0;  // host time blocked on the previous step's planner (since reset)
 };
 
@@ -199,7 +199,9 @@ enum Phase : int {
   kPhRestoreBegin,  // side stream
   kPhRestoreEnd,
   kPhStepBegin,  // top of the forward, before the layout snapshot / H2D
-  kPhCount
+  kPhCount,
+  kPhHistD2H = kPhCount,  // R copied to the host (main stream; extra ring slot)
+  kPhPlanned,             // planner callback done (planner stream; extra ring slot)
 };
 
 // cuStreamWriteValue32 through the runtime's driver entry point (no libcuda link).
@@ -512,6 +514,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   // histogram -> host planner (async, off the critical path)
   CK(cudaMemcpyAsync(L.R_host, L.ranks[0].R_all, static_cast<size_t>(N) * E * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaEventRecord(L.ev_hist, st));
+  mark(L, st, kPhHistD2H);
   if (L.planner) {
     CK(cudaStreamWaitEvent(L.plan_stream, L.ev_hist, 0));
     CK(cudaLaunchHostFunc(
@@ -523,6 +526,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
         },
         &L));
     CK(cudaEventRecord(L.ev_planned, L.plan_stream));
+    mark(L, L.plan_stream, kPhPlanned);
     L.planner_pending = true;
   }
   for (Rank& r : L.ranks)
@@ -1194,6 +1198,19 @@ mp_status mp_fsep_layer_phase_ms(mp_fsep_layer* L, double* out, uint32_t n) {
     for (int i = 0; i < kPhCount; ++i) out[i] = acc[static_cast<size_t>(i)] / static_cast<double>(cnt);
     if (n > static_cast<uint32_t>(kPhCount)) out[kPhCount] = ngap ? gap / static_cast<double>(ngap) : 0.0;
     if (n > static_cast<uint32_t>(kPhCount) + 1) out[kPhCount + 1] = L->host_wait_ms / static_cast<double>(cnt);
+    // out[kPhCount + 2 / + 3]: forward top -> R on the host / -> planner callback done
+    if (n > static_cast<uint32_t>(kPhCount) + 3) {
+      double h = 0.0, pl = 0.0;
+      for (long long s = L->step_no - cnt; s < L->step_no; ++s) {
+        auto& ev = L->ev_p[static_cast<size_t>(s % mp_fsep_layer::kPhaseRing)];
+        float a = 0.f;
+        if (cudaEventElapsedTime(&a, ev[kPhStepBegin], ev[kPhHistD2H]) == cudaSuccess) h += a;
+        if (L->planner && cudaEventElapsedTime(&a, ev[kPhStepBegin], ev[kPhPlanned]) == cudaSuccess) pl += a;
+        cudaGetLastError();
+      }
+      out[kPhCount + 2] = h / static_cast<double>(cnt);
+      out[kPhCount + 3] = pl / static_cast<double>(cnt);
+    }
   });
 }
 
