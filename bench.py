@@ -68,20 +68,25 @@ def zipf_bias(rng, T, E, alpha, perm):
 
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region (the
-    profiling recipe's clocks line, every 50 ms; idle-only samples dropped)."""
+    profiling recipe's clocks line, every 50 ms; idle-only samples dropped).  One
+    nvidia-smi process for all of the job's GPUs, started by local rank 0 only (one
+    poller per rank added host-side jitter at N=4); devices=None: no sampling."""
 
     QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device: int):
-        self.device = device
+    def __init__(self, devices):
+        self.devices = devices
         self.proc = None
 
     def __enter__(self):
+        if self.devices is None:
+            return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
-                                          "-lms", "50", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                          "-lms", "50", "-i", ",".join(str(d) for d in self.devices)],
+                                         stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             time.sleep(0.3)  # let the sampler start (idle-only samples are dropped)
         except FileNotFoundError:
@@ -358,7 +363,8 @@ def main():
 
     # the clock sampler runs from before the warm-up steps to the end of the timed
     # region, so it sees the GPU under load through the whole measured window
-    with ClockSampler(local) as clk:
+    nloc = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    with ClockSampler(list(range(nloc)) if local == 0 else None) as clk:
         for i in range(args.warmup):
             step(i)
         torch.cuda.synchronize()
