@@ -97,14 +97,17 @@ __device__ __forceinline__ void wait_group_ready(const GemmParams& p, int g) {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-__device__ __forceinline__ void wave_barrier(int* ctr, int expected) {
+// Returns false on timeout (~0.4 ms: the CTAs are not all co-resident, e.g. another
+// kernel holds SMs); the caller then stops synchronising for the rest of the launch.
+__device__ __forceinline__ bool wave_barrier(int* ctr, int expected) {
   atomicAdd(ctr, 1);
-  for (int spin = 0; spin < 4000; ++spin) {  // bounded (~0.4 ms): never a hang if CTAs are not co-resident
+  for (int spin = 0; spin < 4000; ++spin) {
     int v;
     asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-    if (v >= expected) break;
+    if (v >= expected) return true;
     __nanosleep(64);
   }
+  return false;
 }
 
 namespace gemm {

@@ -222,9 +222,10 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       int ready_g = -1;
+      bool wsync = p.wave_sync != nullptr;
       for (int w = 0, t = wave_tile(0); t < total_tiles; t = wave_tile(++w)) {
-        if (p.wave_sync != nullptr && w > 0 && w <= kWaveSyncMax)  // CTAs with a tile in wave w
-          wave_barrier(p.wave_sync + (w - 1), 2 * min(nclusters, total_tiles - w * nclusters));
+        if (wsync && w > 0 && w <= kWaveSyncMax)  // CTAs with a tile in wave w
+          wsync = wave_barrier(p.wave_sync + (w - 1), 2 * min(nclusters, total_tiles - w * nclusters));
         int g, mb, nbk;
         decode(t, g, mb, nbk);
         const int nk = k_blocks(g);
