@@ -22,7 +22,10 @@ def rel(a, b):
     return float(np.abs(np.asarray(a, np.float64) - b).max() / max(np.abs(b).max(), 1e-30))
 
 
-@pytest.mark.parametrize("world,E,K,H,F,T,C", [(2, 8, 2, 512, 256, 384, 4), (4, 8, 2, 256, 256, 256, 2)])
+# the top-4 case runs the de-duplicated dispatch (one NVLink transfer per token and
+# destination device) and the slot-by-slot expansion beside the gate-up GEMM
+@pytest.mark.parametrize("world,E,K,H,F,T,C", [(2, 8, 2, 512, 256, 384, 4), (4, 8, 2, 256, 256, 256, 2),
+                                               (4, 16, 4, 512, 256, 512, 8)])
 def test_real_multi_gpu(tmp_path, world, E, K, H, F, T, C):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
