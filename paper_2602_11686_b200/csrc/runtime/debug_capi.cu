@@ -2,6 +2,7 @@
 // device buffers so the kernel can be checked in isolation against a torch fp32
 // matmul (tests/test_gpu_gemm.py).  Not used by the layer step.
 #include "host/capi_common.hpp"
+#include "kernels/fsep_types.cuh"
 #include "kernels/kernels.hpp"
 #include "moeplan_fsep.h"
 
@@ -36,6 +37,10 @@ __attribute__((visibility("default"))) mp_status mp_fsep_debug_grouped_gemm(
     GroupedGemmArgs g{num_groups, group_rows, group_off, M, N, K, out, ldo, out_gstride, out2, ldo2, aux, ld_aux};
     g.policy = (kind >> 12) & 0xF;   // experiment knobs (bits 12-15 policy, 16-23 raster)
     g.raster = (kind >> 16) & 0xFF;
+    static int* wave_sync = nullptr;  // wave-synchronisation counters, as the layer step passes them
+    if (wave_sync == nullptr && cudaMalloc(&wave_sync, kWaveSyncMax * sizeof(int)) != cudaSuccess)
+      throw moeplan::Error(moeplan::ErrorKind::device, "cudaMalloc(wave_sync) failed");
+    g.wave_sync = wave_sync;
     if (pair)
       launch_grouped_gemm_pair(k, ta, tb, g, sms, static_cast<cudaStream_t>(stream));
     else
