@@ -190,7 +190,7 @@ def run_reference_impl(args, cfg):
 
 
 # ---------------------------------------------------------------- GPU path
-def token_kernel_bandwidth(phases, layer, PL, N, rank, T, K, H):
+def token_kernel_bandwidth(phases, layer, PL, N, rank, T, K, H, F=0, C=0):
     """HBM and NVLink throughput of the token-movement kernels (rank 0's layer 0).
 
     Algorithmic bytes per step (bf16 rows of H elements, T tokens, K slots each):
@@ -199,6 +199,10 @@ def token_kernel_bandwidth(phases, layer, PL, N, rank, T, K, H):
       unpermute   read T*K dx rows (local/peer) + write dx (T*H*2)
     The remote share (rows whose slot lives on another GPU, i.e. NVLink traffic)
     comes from lite_routing(R, A) of the step's histogram and layout.
+    With F and C (N > 1): the shard restore, C hosted experts x (N-1)/N of their
+    3*H*F bf16 parameters received over NVLink per step (copy-engine pushes), over
+    the restore's issue-to-join interval (a lower bound on its rate: it runs under
+    the forward and the interval includes the wait for the join).
     """
     row = H * 2
     remote = 0
@@ -223,6 +227,11 @@ def token_kernel_bandwidth(phases, layer, PL, N, rank, T, K, H):
     hbm = peaks()[2]
     for v in out.values():
         v["hbm_frac"] = round(v["GBps"] / hbm, 4)
+    rms = phases.get("restore_ms") or 0.0
+    if N > 1 and F and C and rms > 0:
+        b = C * 3 * H * F * 2 * (N - 1) // N
+        out["restore"] = {"ms": round(rms, 4), "bytes": b, "nvlink_GBps": round(b / (rms * 1e-3) / 1e9, 1),
+                          "note": "copy-engine pushes under the forward; issue-to-join interval"}
     return out
 
 
@@ -376,7 +385,7 @@ def main():
     phases = layers[0].phase_ms() if os.environ.get("FSEP_PHASE_TIMING") == "1" else None
     if phases:
         phases["fwd_gemms"] = round(phases["fwd_gemm_gateup"] + phases["fwd_gemm_down"], 4)
-    comm = token_kernel_bandwidth(phases, layers[0], PL, N, rank, T, K, H) if phases else None
+    comm = token_kernel_bandwidth(phases, layers[0], PL, N, rank, T, K, H, F, C) if phases else None
     per_rank = None
     if world > 1 and phases:
         # per-rank view of the phases that expose load imbalance (barrier waits absorb it)

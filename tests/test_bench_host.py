@@ -62,6 +62,11 @@ def test_token_kernel_bytes_and_remote_rows():
     lf = bench.token_kernel_bandwidth(phases, _FakeLayer(R, A, local_first=True), PL, N, 0, T, K, H)
     # local-first keeps the tokens of experts 0, 1, 3 (hosted on rank 0) local
     assert lf["dispatch"]["remote_rows"] == int(R[0, 2])
+    # shard restore: C hosted experts x (N-1)/N of 3HF bf16 parameters over the issue-to-join time
+    F, C = 512, 3
+    rs = bench.token_kernel_bandwidth(dict(phases, restore_ms=2.0), _FakeLayer(R, A), PL, N, 0, T, K, H, F, C)
+    assert rs["restore"]["bytes"] == C * 3 * H * F * 2 * (N - 1) // N
+    assert rs["restore"]["nvlink_GBps"] == round(rs["restore"]["bytes"] / 2e-3 / 1e9, 1)
 
 
 def test_calibrated_config_runs_reference_analysis():
