@@ -201,8 +201,8 @@ def token_kernel_bandwidth(phases, layer, PL, N, rank, T, K, H, F=0, C=0):
     comes from lite_routing(R, A) of the step's histogram and layout.
     With F and C (N > 1): the shard restore, C hosted experts x (N-1)/N of their
     3*H*F bf16 parameters received over NVLink per step (copy-engine pushes), over
-    the restore's issue-to-join interval (a lower bound on its rate: it runs under
-    the forward and the interval includes the wait for the join).
+    the time from the restore's start to its last push landing (phase
+    restore_landed_ms; else the issue-to-join interval, a lower bound on the rate).
     """
     row = H * 2
     remote = 0
@@ -227,11 +227,13 @@ def token_kernel_bandwidth(phases, layer, PL, N, rank, T, K, H, F=0, C=0):
     hbm = peaks()[2]
     for v in out.values():
         v["hbm_frac"] = round(v["GBps"] / hbm, 4)
-    rms = phases.get("restore_ms") or 0.0
+    rms = phases.get("restore_landed_ms") or phases.get("restore_ms") or 0.0
     if N > 1 and F and C and rms > 0:
         b = C * 3 * H * F * 2 * (N - 1) // N
         out["restore"] = {"ms": round(rms, 4), "bytes": b, "nvlink_GBps": round(b / (rms * 1e-3) / 1e9, 1),
-                          "note": "copy-engine pushes under the forward; issue-to-join interval"}
+                          "note": "copy-engine pushes under the forward; restore begin -> last push landed"
+                                  if phases.get("restore_landed_ms") else
+                                  "copy-engine pushes under the forward; issue-to-join interval"}
     return out
 
 

@@ -206,7 +206,8 @@ mp_status mp_fsep_layer_stats_reset(mp_fsep_layer* layer);
  * restore issue-to-join time; out[22] forward top -> first phase (layout
  * snapshot + H2D); out[23] idle gap between the previous step's end and this
  * step's top; out[24] host time blocked on the planner per step; out[25] / out[26]
- * forward top -> histogram on the host / -> planner callback done.  n >= 23. */
+ * forward top -> histogram on the host / -> planner callback done; out[27] restore
+ * begin -> last copy-engine restore push landed.  n >= 23. */
 mp_status mp_fsep_layer_phase_ms(mp_fsep_layer* layer, double* out, uint32_t n);
 
 /* Capture forward+backward into a CUDA graph and replay it (bench path). */

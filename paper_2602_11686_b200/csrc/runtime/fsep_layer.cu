@@ -171,6 +171,7 @@ extern "C" struct mp_fsep_layer {
   static constexpr int kPhaseRing = 64;
   bool phase_on = false;
   std::vector<std::array<cudaEvent_t, 26>> ev_p;
+  std::vector<std::array<cudaEvent_t, kMaxRanks>> ev_ce_t;  // per step: last restore push to each peer landed
   double host_wait_ms = 0.0;  // host time blocked on the previous step's planner (since reset)
 };
 
@@ -449,6 +450,7 @@ void push_restore(Layer& L, cudaStream_t st, int c0 = 0, int c1 = kMaxExperts) {
         throw Error(ErrorKind::device, "cuStreamWriteValue32 failed");
     }
     CK(cudaEventRecord(L.ev_ce[d], L.ce[d]));
+    if (L.phase_on) cudaEventRecord(L.ev_ce_t[static_cast<size_t>(L.step_no % mp_fsep_layer::kPhaseRing)][d], L.ce[d]);
   }
 }
 
@@ -812,6 +814,9 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
       L->phase_on = true;
       L->ev_p.resize(mp_fsep_layer::kPhaseRing);
       for (auto& ring : L->ev_p)
+        for (auto& e : ring) CK(cudaEventCreate(&e));
+      L->ev_ce_t.resize(mp_fsep_layer::kPhaseRing);
+      for (auto& ring : L->ev_ce_t)
         for (auto& e : ring) CK(cudaEventCreate(&e));
     }
     if (const char* v = std::getenv("FSEP_RESTORE_BLOCKS")) L->restore_blocks = std::max(1, std::atoi(v));
@@ -1198,6 +1203,25 @@ mp_status mp_fsep_layer_phase_ms(mp_fsep_layer* L, double* out, uint32_t n) {
     for (int i = 0; i < kPhCount; ++i) out[i] = acc[static_cast<size_t>(i)] / static_cast<double>(cnt);
     if (n > static_cast<uint32_t>(kPhCount)) out[kPhCount] = ngap ? gap / static_cast<double>(ngap) : 0.0;
     if (n > static_cast<uint32_t>(kPhCount) + 1) out[kPhCount + 1] = L->host_wait_ms / static_cast<double>(cnt);
+    // out[kPhCount + 4]: restore begin -> last copy-engine push landed (copy-engine mode)
+    if (n > static_cast<uint32_t>(kPhCount) + 4) {
+      double land = 0.0;
+      long long nl = 0;
+      for (long long s = L->step_no - cnt; s < L->step_no && L->ce_mode && restore; ++s) {
+        auto& ev = L->ev_p[static_cast<size_t>(s % mp_fsep_layer::kPhaseRing)];
+        auto& ce = L->ev_ce_t[static_cast<size_t>(s % mp_fsep_layer::kPhaseRing)];
+        float mx = 0.f;
+        bool ok = false;
+        for (int d = 0; d < L->N; ++d) {
+          if (d == L->ranks[0].rank) continue;
+          float a = 0.f;
+          if (cudaEventElapsedTime(&a, ev[kPhRestoreBegin], ce[d]) == cudaSuccess) mx = std::max(mx, a), ok = true;
+        }
+        cudaGetLastError();
+        if (ok) land += mx, ++nl;
+      }
+      out[kPhCount + 4] = nl ? land / static_cast<double>(nl) : 0.0;
+    }
     // out[kPhCount + 2 / + 3]: forward top -> R on the host / -> planner callback done
     if (n > static_cast<uint32_t>(kPhCount) + 3) {
       double h = 0.0, pl = 0.0;

@@ -166,7 +166,7 @@ class FsepLayer:
     PHASES = ["param_barrier", "router_scan", "R_barrier", "plan", "dispatch", "dispatch_barrier", "restore_wait",
               "fwd_gemm_gateup", "fwd_gemm_down", "fwd_barrier", "combine", "combine_bwd_router_wgrad", "bwd_barrier0", "bwd_gemms",
               "rs_push_wait", "rs_barrier", "rs_sum", "unpermute", "grad_reduce_scatter_kernel", "step_total", "restore_start",
-              "restore_ms", "layout_h2d", "gap_between_steps", "host_planner_wait", "hist_on_host_at", "planner_done_at"]
+              "restore_ms", "layout_h2d", "gap_between_steps", "host_planner_wait", "hist_on_host_at", "planner_done_at", "restore_landed_ms"]
 
     def phase_ms(self):
         """Mean per-phase device times (needs FSEP_PHASE_TIMING=1 at layer creation), or None."""
