@@ -118,6 +118,14 @@ typedef struct mp_fsep_desc {
  * one NVSwitch node; replica loads stay near-balanced when ranks see similar
  * routing distributions. */
 #define MP_FSEP_FLAG_LOCAL_FIRST 2u
+/* Virtual mode only: run the real multi-GPU transport between the emulated
+ * ranks -- copy-engine shard-restore pushes, each followed by a
+ * cuStreamWriteValue32 readiness flag polled per (slot, source) by the gate-up
+ * GEMM's producer, copy-engine gradient pushes into the owners' staging rows and
+ * the owner-side ascending-device sum -- instead of the device-side restore /
+ * reduce-scatter kernels.  This is how one GPU checks the shipped N>1 data plane
+ * against the oracle (real mode always uses it unless FSEP_COMM=kernel). */
+#define MP_FSEP_FLAG_COPY_ENGINE 4u
 
 mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_layer** out);
 void mp_fsep_layer_free(mp_fsep_layer* layer);
@@ -209,6 +217,23 @@ mp_status mp_fsep_layer_stats_reset(mp_fsep_layer* layer);
  * forward top -> histogram on the host / -> planner callback done; out[27] restore
  * begin -> last copy-engine restore push landed.  n >= 23. */
 mp_status mp_fsep_layer_phase_ms(mp_fsep_layer* layer, double* out, uint32_t n);
+
+/* Device-detected failures.  Kernels record them in host-mapped words:
+ *   bit 0  receive-buffer overflow (a segment exceeded max_recv_rows; dropped),
+ *   bit 1  peer barrier timeout (a rank did not arrive within FSEP_SPIN_TIMEOUT_MS,
+ *          default 10 s),
+ *   bit 2  restore readiness timeout (a restored expert chunk's flag never
+ *          arrived; the gate-up GEMM stopped waiting).
+ * Every mp_fsep_layer_forward / _backward / _graph_step / _stats call first
+ * reports the words that have landed (MP_ERR_DEVICE, message naming the causes,
+ * words cleared).  mp_fsep_layer_check synchronises the device first, so it sees
+ * every step enqueued so far; *bits (may be NULL) gets the set bits.  Like every
+ * error of this ABI (capi.cpp:54-70), the failure is returned, never thrown. */
+mp_status mp_fsep_layer_check(mp_fsep_layer* layer, uint32_t* bits);
+/* Test hook forcing a failure condition: "drop_restore_flag" (copy-engine mode:
+ * the next restore skips one readiness flag -> bit 2), "barrier_timeout"
+ * (virtual mode: emulated rank 0 enters a peer barrier alone -> bit 1). */
+mp_status mp_fsep_layer_debug_inject(mp_fsep_layer* layer, const char* what);
 
 /* Capture forward+backward into a CUDA graph and replay it (bench path). */
 mp_status mp_fsep_layer_graph_step(mp_fsep_layer* layer, const void* x, const float* bias, uint32_t n_tokens,

@@ -98,6 +98,8 @@ _SIGS = {
     "mp_fsep_layer_stats_reset": (C.c_int, [vp]),
     "mp_fsep_layer_phase_ms": (C.c_int, [vp, dblp, u32]),
     "mp_fsep_layer_graph_step": (C.c_int, [vp, vp, vp, u32, vp, vp, vp, vp]),
+    "mp_fsep_layer_check": (C.c_int, [vp, C.POINTER(u32)]),
+    "mp_fsep_layer_debug_inject": (C.c_int, [vp, cp]),
 }
 
 

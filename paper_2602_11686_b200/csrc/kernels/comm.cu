@@ -50,23 +50,25 @@ __global__ void __launch_bounds__(256) restore_kernel(const uint8_t* __restrict_
 
 // All-rank barrier: publish `epoch` into every peer's slot for this rank, then
 // wait until every rank has published it here.  System-scope release/acquire
-// orders the preceding peer stores of the step.  Bounded spin: on timeout the
-// kernel records the failure in flags[world] and returns (no trap).
+// orders the preceding peer stores of the step.  Bounded: after timeout_ns the
+// kernel raises kErrBarrierTimeout (host-mapped, reported by the next
+// mp_fsep_layer_* call as MP_ERR_DEVICE), records flags[world] and returns.
 __global__ void peer_barrier_kernel(unsigned int* const* __restrict__ peer_flags, int world, int rank,
-                                    unsigned int epoch) {
+                                    unsigned int epoch, unsigned* err, unsigned long long timeout_ns) {
   const int p = threadIdx.x;
   if (p < world) {
     unsigned int* slot = peer_flags[p] + rank;
     asm volatile("fence.acq_rel.sys;" ::: "memory");
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(slot), "r"(epoch) : "memory");
     const unsigned int* mine = peer_flags[rank] + p;
-    unsigned int v = 0;
-    long long spins = 0;
+    const unsigned long long t0 = globaltimer_ns();
     while (true) {
+      unsigned int v;
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
       if (static_cast<int>(v - epoch) >= 0) break;
-      if (++spins > (1LL << 26)) {  // ~ seconds
+      if (globaltimer_ns() - t0 > timeout_ns) {
         atomicOr(peer_flags[rank] + world, 1u);
+        raise_err(err, kErrBarrierTimeout);
         break;
       }
       __nanosleep(64);
@@ -83,8 +85,9 @@ void launch_restore(const uint8_t* layout, int E, int N, int rank, int C, long l
   count_launch();
 }
 
-void launch_peer_barrier(unsigned int* const* peer_flags, int world, int rank, unsigned int epoch, cudaStream_t st) {
-  peer_barrier_kernel<<<1, 32, 0, st>>>(peer_flags, world, rank, epoch);
+void launch_peer_barrier(unsigned int* const* peer_flags, int world, int rank, unsigned int epoch, unsigned* err,
+                         unsigned long long timeout_ns, cudaStream_t st) {
+  peer_barrier_kernel<<<1, 32, 0, st>>>(peer_flags, world, rank, epoch, err, timeout_ns);
   count_launch();
 }
 

@@ -45,6 +45,27 @@ struct PeerTable {
   uint64_t row_capacity;                 // rows of every receive buffer
 };
 
+// Device-detected step failures.  Each cause has its own word in host-mapped
+// pinned memory (plain system-scope stores of 1: no host atomics needed over
+// PCIe); the runtime reports a set word as MP_ERR_DEVICE at the next
+// mp_fsep_layer_* call (mp_fsep_layer_check synchronises first).
+enum ErrWord : int {
+  kErrRecvOverflow = 0,     // a receive segment did not fit max_recv_rows (segments dropped)
+  kErrBarrierTimeout = 1,   // a peer barrier timed out (a rank did not arrive)
+  kErrRestoreTimeout = 2,   // a restored expert chunk's readiness flag never arrived
+  kErrWords = 4,
+};
+__device__ __forceinline__ void raise_err(unsigned* err, int word) {
+  if (err == nullptr) return;
+  *reinterpret_cast<volatile unsigned*>(err + word) = 1u;
+  __threadfence_system();
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 struct PlanTables {
   // global view (identical on all ranks)
   int n_hosts[kMaxExperts];

@@ -126,7 +126,7 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
   if (!pair_gemm_supported(kind, a)) throw std::runtime_error("pair gemm: wgrad M must be a multiple of 256");
   GemmParams p{a.num_groups, a.group_rows, a.group_off, a.M,    a.N,    a.K,   a.out,
                a.ldo,        a.out_group_stride, a.out2,    a.ldo2, a.aux, a.ld_aux, a.policy, a.raster,
-               a.ready,      a.ready_epoch,      a.ready_n,
+               a.ready,      a.ready_epoch,      a.ready_n,      a.err, a.ready_timeout_ns,
                a.row_src,    a.scatter,          a.scatter_rows, nullptr};
   static const bool wave_sync = [] {  // FSEP_WAVE_SYNC=0: free-running producers
     const char* v = std::getenv("FSEP_WAVE_SYNC");
@@ -186,7 +186,7 @@ void launch_grouped_gemm(GemmKind kind, const CUtensorMap& tmA, const CUtensorMa
   if (a.N % 32 != 0) throw std::runtime_error("grouped gemm: N must be a multiple of 32");
   GemmParams p{a.num_groups, a.group_rows, a.group_off, a.M,    a.N,    a.K,   a.out,
                a.ldo,        a.out_group_stride, a.out2,    a.ldo2, a.aux, a.ld_aux, a.policy, a.raster,
-               a.ready,      a.ready_epoch,      a.ready_n,
+               a.ready,      a.ready_epoch,      a.ready_n,      a.err, a.ready_timeout_ns,
                a.row_src,    a.scatter,          a.scatter_rows, nullptr};
   switch (kind) {
     case GemmKind::kFwdGateUp: launch_one<false, false, false, kEpiSwigluFwd>(tmA, tmB, p, num_sms, stream); break;

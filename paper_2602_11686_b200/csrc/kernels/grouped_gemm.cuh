@@ -58,6 +58,10 @@ struct GemmParams {
   const unsigned* ready;
   unsigned ready_epoch;
   int ready_n;
+  // Bounded wait: after ready_timeout_ns without the flag the producer raises
+  // kErrRestoreTimeout in err (host-mapped) and stops waiting for the launch.
+  unsigned* err;
+  unsigned long long ready_timeout_ns;
   // Optional row scatter (kEpiBf16, M-grouped): output row r is stored to
   // scatter[code >> 26] + (code & 0x3FFFFFF) * ldo, code = row_src[r] (code < 0:
   // padding row, not stored).  This is how the expert outputs travel straight
@@ -82,19 +86,27 @@ __device__ __forceinline__ __nv_bfloat16* bf16_out_row(const GemmParams& p, long
   return p.scatter[code >> 26] + idx * p.ldo;
 }
 
-__device__ __forceinline__ void wait_group_ready(const GemmParams& p, int g) {
-  if (p.ready == nullptr) return;
+// The flags are written by the pushing peers' copy engines (another GPU in real
+// mode): system-scope acquire.  Returns false after a timeout (error raised).
+__device__ __forceinline__ bool wait_group_ready(const GemmParams& p, int g) {
+  if (p.ready == nullptr) return true;
+  const unsigned long long t0 = globaltimer_ns();
   for (int q = 0; q < p.ready_n; ++q) {
     const unsigned* f = p.ready + g * p.ready_n + q;
     while (true) {
       unsigned v;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
       if (static_cast<int>(v - p.ready_epoch) >= 0) break;
+      if (globaltimer_ns() - t0 > p.ready_timeout_ns) {
+        raise_err(p.err, kErrRestoreTimeout);
+        return false;
+      }
       __nanosleep(256);
     }
   }
   // the chunks were written by copy engines (generic proxy); TMA reads via the async proxy
   asm volatile("fence.proxy.async.global;" ::: "memory");
+  return true;
 }
 
 // Returns false on timeout (~0.4 ms: the CTAs are not all co-resident, e.g. another
@@ -232,13 +244,14 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       int ready_g = -1;
+      bool ready_live = true;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         int g, mb, nbk;
         decode(t, g, mb, nbk);
         const int nk = k_blocks(g);
         const int row0 = p.group_off[g];
-        if (!kGroupK && g != ready_g) {
-          wait_group_ready(p, g);
+        if (!kGroupK && g != ready_g && ready_live) {
+          ready_live = wait_group_ready(p, g);  // false: timed out (error raised), stop waiting
           ready_g = g;
         }
         for (int kb = 0; kb < nk; ++kb) {

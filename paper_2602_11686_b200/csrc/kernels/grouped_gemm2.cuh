@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       int ready_g = -1;
+      bool ready_live = true;
       bool wsync = p.wave_sync != nullptr;
       for (int w = 0, t = wave_tile(0); t < total_tiles; t = wave_tile(++w)) {
         if (wsync && w > 0 && w <= kWaveSyncMax)  // CTAs with a tile in wave w
@@ -230,8 +231,8 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
         decode(t, g, mb, nbk);
         const int nk = k_blocks(g);
         const int row0 = p.group_off[g];
-        if (!kGroupK && g != ready_g) {
-          wait_group_ready(p, g);
+        if (!kGroupK && g != ready_g && ready_live) {
+          ready_live = wait_group_ready(p, g);  // false: timed out (error raised), stop waiting
           ready_g = g;
         }
         const int m_half = mb * BM + rank * HALF;   // this CTA's first A row (M-grouped: within the group)

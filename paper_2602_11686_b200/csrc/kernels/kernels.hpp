@@ -35,6 +35,8 @@ struct GroupedGemmArgs {
   const unsigned* ready = nullptr;  // per-group readiness flags (see GemmParams)
   unsigned ready_epoch = 0;
   int ready_n = 0;
+  unsigned* err = nullptr;  // host-mapped error words (fsep_types.cuh ErrWord)
+  unsigned long long ready_timeout_ns = 10000000000ull;
   const int* row_src = nullptr;  // optional row scatter of the bf16 epilogue (see GemmParams)
   __nv_bfloat16* const* scatter = nullptr;
   long long scatter_rows = 0;

@@ -102,7 +102,8 @@ __device__ __forceinline__ long long route_amount(const unsigned long long* R_al
 }
 
 __global__ void plan_kernel(const unsigned long long* __restrict__ R_all, const uint8_t* __restrict__ layout, int E,
-                            int N, int rank, PlanTables* __restrict__ pt, long long row_capacity, bool local_first) {
+                            int N, int rank, PlanTables* __restrict__ pt, long long row_capacity, bool local_first,
+                            unsigned* err) {
   __shared__ int s_seg_off[kMaxRanks][kMaxExperts];
   const int tid = threadIdx.x;
   for (int e = tid; e < E; e += blockDim.x) {
@@ -143,6 +144,7 @@ __global__ void plan_kernel(const unsigned long long* __restrict__ R_all, const 
     if (d == rank) {
       pt->total_rows = static_cast<int>(off);
       pt->status = off > row_capacity ? 1 : 0;
+      if (off > row_capacity) raise_err(err, kErrRecvOverflow);
     }
   }
   __syncthreads();
@@ -705,8 +707,8 @@ void launch_block_scan(const int* blk_hist, int nblk, int E, int* blk_base, cons
 }
 
 void launch_plan(const unsigned long long* R_all, const uint8_t* layout, int E, int N, int rank, PlanTables* pt,
-                 long long row_capacity, bool local_first, cudaStream_t st) {
-  plan_kernel<<<1, 128, 0, st>>>(R_all, layout, E, N, rank, pt, row_capacity, local_first);
+                 long long row_capacity, bool local_first, unsigned* err, cudaStream_t st) {
+  plan_kernel<<<1, 128, 0, st>>>(R_all, layout, E, N, rank, pt, row_capacity, local_first, err);
   count_launch();
 }
 

@@ -39,7 +39,7 @@ void launch_router(const RouterArgs& a, cudaStream_t st);
 void launch_block_scan(const int* blk_hist, int nblk, int E, int* blk_base, const PeerTable& peers, int rank,
                        int world, cudaStream_t st);
 void launch_plan(const unsigned long long* R_all, const uint8_t* layout, int E, int N, int rank, PlanTables* pt,
-                 long long row_capacity, bool local_first, cudaStream_t st);
+                 long long row_capacity, bool local_first, unsigned* err, cudaStream_t st);
 void launch_zero_pad(const PlanTables* pt, int C, int H, __nv_bfloat16* x_rows, __nv_bfloat16* dy_rows,
                      int* row_src, cudaStream_t st);
 void launch_dispatch(const DispatchArgs& a, cudaStream_t st);
@@ -74,6 +74,8 @@ void launch_restore(const uint8_t* layout, int E, int N, int rank, int C, long l
                     const PeerTable& peers, __nv_bfloat16* restored, int blocks_per_chunk, cudaStream_t st);
 
 // Cross-rank barrier for real multi-GPU mode (system-scope flags in peer memory).
-void launch_peer_barrier(unsigned int* const* peer_flags, int world, int rank, unsigned int epoch, cudaStream_t st);
+// Bounded: after timeout_ns the kernel raises kErrBarrierTimeout in err (and flags[world]) and returns.
+void launch_peer_barrier(unsigned int* const* peer_flags, int world, int rank, unsigned int epoch, unsigned* err,
+                         unsigned long long timeout_ns, cudaStream_t st);
 
 }  // namespace fsep

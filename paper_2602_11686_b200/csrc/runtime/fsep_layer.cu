@@ -144,7 +144,7 @@ extern "C" struct mp_fsep_layer {
   bool restore_dirty = true;   // resident mode: hosted experts must be (re)restored
   bool local_first = false;    // MP_FSEP_FLAG_LOCAL_FIRST (non-parity routing variant)
   bool dedupe = false;         // token rows cross NVLink once per destination device (K >= 4)
-  mp_fsep_layer* next = nullptr;  // chained next layer: its restore is issued after this layer's dispatch
+  mp_fsep_layer* next = nullptr;  // chained next layer: its restore is issued after this layer's gate-up GEMM
   bool prefetched = false;        // this layer's restore for the coming forward is already in flight
   bool restore_split = true;      // push slot 0 before dispatch, the rest after (FSEP_RESTORE_SPLIT=0: all before)
   // graph
@@ -173,6 +173,12 @@ extern "C" struct mp_fsep_layer {
   std::vector<std::array<cudaEvent_t, 26>> ev_p;
   std::vector<std::array<cudaEvent_t, kMaxRanks>> ev_ce_t;  // per step: last restore push to each peer landed
   double host_wait_ms = 0.0;  // host time blocked on the previous step's planner (since reset)
+  // device-detected failures (fsep_types.cuh ErrWord): host-mapped words, one per cause
+  unsigned* err_host = nullptr;
+  unsigned* err_dev = nullptr;
+  unsigned long long spin_timeout_ns = 10000000000ull;  // FSEP_SPIN_TIMEOUT_MS (barriers, readiness waits)
+  int drop_flag = -1;  // test hook (mp_fsep_layer_debug_inject "drop_restore_flag"): source rank whose
+                       // next slot-0 readiness flag is not written
 };
 
 namespace {
@@ -373,6 +379,11 @@ void finish_peers(Layer& L) {
       L.peers.R_all[p] = r.R_all;
       L.peers.grad_full[p] = r.grad_full;
       L.peers.shard[p] = r.shard;
+      if (L.ce_mode) {  // virtual copy-engine mode: push targets are the emulated ranks' arenas
+        L.peer_restored[p] = r.restored;
+        L.peer_ready[p] = r.ready;
+        L.peer_rs_stage[p] = r.rs_stage;
+      }
     }
   }
   L.peers.row_capacity = static_cast<uint64_t>(L.cap);
@@ -380,7 +391,7 @@ void finish_peers(Layer& L) {
 
 void barrier(Layer& L, cudaStream_t st) {
   if (L.virt || L.N == 1) return;  // stream order is the barrier on one GPU
-  launch_peer_barrier(L.d_peer_flags, L.N, L.ranks[0].rank, ++L.epoch, st);
+  launch_peer_barrier(L.d_peer_flags, L.N, L.ranks[0].rank, ++L.epoch, L.err_dev, L.spin_timeout_ns, st);
 }
 
 // CTA-pair (cta_group::2) kernel by default; FSEP_GEMM=single forces the 128x256 single-CTA kernel.
@@ -406,6 +417,8 @@ GroupedGemmArgs gemm_args(Layer& L, Rank& r) {
   g.group_rows = r.pt->seg_rows_pad;
   g.group_off = r.pt->seg_off;
   g.wave_sync = r.wave_sync;
+  g.err = L.err_dev;
+  g.ready_timeout_ns = L.spin_timeout_ns;
   return g;
 }
 
@@ -424,31 +437,41 @@ void snapshot_layout(Layer& L, cudaStream_t st) {
   for (Rank& r : L.ranks) CK(cudaMemcpyAsync(r.layout_dev, snap, static_cast<size_t>(E) * N, cudaMemcpyHostToDevice, st));
 }
 
-// Push restore: this rank's chunk of every expert goes straight into the
+// Push restore: each local rank's chunk of every expert goes straight into the
 // restored slot of each rank that hosts it (own slots first), and a flag written
 // into the destination's memory after each copy releases that (slot, source)
 // pair to the destination's gate-up GEMM producer.  Ordered after `st`'s work.
 // Slots [c0, c1) of every destination; c0 == 0 opens a new restore epoch.
+// Real mode: one local rank, one copy-engine stream per destination GPU.
+// Virtual mode (MP_FSEP_FLAG_COPY_ENGINE): the same copies and flags between the
+// emulated ranks' arenas on one GPU, stream ce[d] carrying every push into d.
 void push_restore(Layer& L, cudaStream_t st, int c0 = 0, int c1 = kMaxExperts) {
   const int E = L.E, N = L.N;
-  Rank& r = L.ranks[0];
   if (c0 == 0) {
     ++L.restore_epoch;
     mark(L, st, kPhRestoreBegin);
   }
   CK(cudaEventRecord(L.ev_fork, st));
-  for (int q = 0; q < N; ++q) {
-    const int d = (r.rank + q) % N;
-    const std::vector<int> theirs = hosted_experts(L.cur_layout, E, N, d);
-    CK(cudaStreamWaitEvent(L.ce[d], L.ev_fork, 0));
-    for (int c = c0; c < std::min(c1, static_cast<int>(theirs.size())); ++c) {
-      CK(cudaMemcpyAsync(L.peer_restored[d] + static_cast<long long>(c) * L.flat + static_cast<long long>(r.rank) * L.S,
-                         r.shard + static_cast<long long>(theirs[c]) * L.S, static_cast<size_t>(L.S) * 2,
-                         cudaMemcpyDeviceToDevice, L.ce[d]));
-      if (write_value_fn()(L.ce[d], reinterpret_cast<CUdeviceptr>(L.peer_ready[d] + c * N + r.rank), L.restore_epoch,
-                           0) != CUDA_SUCCESS)
-        throw Error(ErrorKind::device, "cuStreamWriteValue32 failed");
+  for (int d = 0; d < N; ++d) CK(cudaStreamWaitEvent(L.ce[d], L.ev_fork, 0));
+  for (Rank& r : L.ranks) {
+    for (int q = 0; q < N; ++q) {
+      const int d = (r.rank + q) % N;
+      const std::vector<int> theirs = hosted_experts(L.cur_layout, E, N, d);
+      for (int c = c0; c < std::min(c1, static_cast<int>(theirs.size())); ++c) {
+        CK(cudaMemcpyAsync(L.peer_restored[d] + static_cast<long long>(c) * L.flat + static_cast<long long>(r.rank) * L.S,
+                           r.shard + static_cast<long long>(theirs[c]) * L.S, static_cast<size_t>(L.S) * 2,
+                           cudaMemcpyDeviceToDevice, L.ce[d]));
+        if (c == 0 && L.drop_flag == r.rank && d != r.rank) {  // test hook: this flag never arrives
+          L.drop_flag = -1;
+          continue;
+        }
+        if (write_value_fn()(L.ce[d], reinterpret_cast<CUdeviceptr>(L.peer_ready[d] + c * N + r.rank),
+                             L.restore_epoch, 0) != CUDA_SUCCESS)
+          throw Error(ErrorKind::device, "cuStreamWriteValue32 failed");
+      }
     }
+  }
+  for (int d = 0; d < N; ++d) {
     CK(cudaEventRecord(L.ev_ce[d], L.ce[d]));
     if (L.phase_on) cudaEventRecord(L.ev_ce_t[static_cast<size_t>(L.step_no % mp_fsep_layer::kPhaseRing)][d], L.ce[d]);
   }
@@ -509,7 +532,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   mark(L, st, kPhRBarrier);
   // 4. device lite routing + receive layout; dispatch
   for (Rank& r : L.ranks) {
-    launch_plan(r.R_all, r.layout_dev, E, N, r.rank, r.pt, L.cap, L.local_first, st);
+    launch_plan(r.R_all, r.layout_dev, E, N, r.rank, r.pt, L.cap, L.local_first, L.err_dev, st);
     launch_zero_pad(r.pt, C, H, r.x_rows, r.dy_rows, r.row_src, st);
   }
   mark(L, st, kPhPlan);
@@ -627,20 +650,21 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   // Push this rank's replica-gradient chunks [lo, hi) of the flat vector to their
   // owners' staging rows (copy engines, one stream per owner), after `ev`.
   auto push_grads = [&](cudaEvent_t ev, long long lo, long long hi) {
-    Rank& r = L.ranks[0];
-    const std::vector<int> mine = hosted_experts(L.cur_layout, E, N, r.rank);
-    for (int q = 1; q < N; ++q) {
-      const int o = (r.rank + q) % N;
-      const long long a = std::max(lo, static_cast<long long>(o) * L.S);
-      const long long b = std::min(hi, static_cast<long long>(o + 1) * L.S);
-      if (a >= b) continue;
-      CK(cudaStreamWaitEvent(L.ce[o], ev, 0));
-      for (int c = 0; c < static_cast<int>(mine.size()); ++c)
-        CK(cudaMemcpyAsync(L.peer_rs_stage[o] + (static_cast<long long>(mine[c]) * N + r.rank) * L.S + (a - o * L.S),
-                           r.grad_full + static_cast<long long>(c) * L.flat + a, static_cast<size_t>(b - a) * 4,
-                           cudaMemcpyDeviceToDevice, L.ce[o]));
-      CK(cudaEventRecord(L.ev_ce[o], L.ce[o]));
+    for (int o = 0; o < N; ++o) CK(cudaStreamWaitEvent(L.ce[o], ev, 0));
+    for (Rank& r : L.ranks) {
+      const std::vector<int> mine = hosted_experts(L.cur_layout, E, N, r.rank);
+      for (int q = 1; q < N; ++q) {
+        const int o = (r.rank + q) % N;
+        const long long a = std::max(lo, static_cast<long long>(o) * L.S);
+        const long long b = std::min(hi, static_cast<long long>(o + 1) * L.S);
+        if (a >= b) continue;
+        for (int c = 0; c < static_cast<int>(mine.size()); ++c)
+          CK(cudaMemcpyAsync(L.peer_rs_stage[o] + (static_cast<long long>(mine[c]) * N + r.rank) * L.S + (a - o * L.S),
+                             r.grad_full + static_cast<long long>(c) * L.flat + a, static_cast<size_t>(b - a) * 4,
+                             cudaMemcpyDeviceToDevice, L.ce[o]));
+      }
     }
+    for (int o = 0; o < N; ++o) CK(cudaEventRecord(L.ev_ce[o], L.ce[o]));
   };
   const long long w2_lo = 2LL * F * H;
   // Order: dH (SwiGLU' fused), dW13, dW2, dX.  The W13 part of the replica
@@ -694,14 +718,14 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][3], st));
   mark(L, st, kPhBwdGemm);
   if (ce_rs) {
-    Rank& r = L.ranks[0];
-    for (int q = 1; q < N; ++q) CK(cudaStreamWaitEvent(st, L.ev_ce[(r.rank + q) % N], 0));  // own pushes landed
+    for (int o = 0; o < N; ++o) CK(cudaStreamWaitEvent(st, L.ev_ce[o], 0));  // own pushes landed
     mark(L, st, kPhRsPushWait);
     // ... and everyone else's: this barrier also orders every rank's dX GEMM (whose
     // epilogue stored dX rows into our tok_rows) before the unpermute below
     barrier(L, st);
     mark(L, st, kPhRsBarrier);
-    launch_grad_rs_sum(r.pt, r.grad_full, r.rs_stage, E, N, r.rank, L.S, L.flat, r.grad_shard, st);
+    for (Rank& r : L.ranks)
+      launch_grad_rs_sum(r.pt, r.grad_full, r.rs_stage, E, N, r.rank, L.S, L.flat, r.grad_shard, st);
   } else {
     mark(L, st, kPhRsPushWait);
     barrier(L, st);
@@ -726,6 +750,29 @@ Rank& rank_of(Layer& L, uint32_t vrank) {
   if (vrank >= L.ranks.size()) throw Error(ErrorKind::invalid_argument, "vrank out of range");
   return L.ranks[vrank];
 }
+
+// Device-detected failures that have landed in the host-mapped words so far:
+// report (MP_ERR_DEVICE, naming the causes) and clear them.  `bits` gets
+// 1 << ErrWord for every set word.
+uint32_t take_errors(Layer& L) {
+  uint32_t bits = 0;
+  for (int w = 0; w < kErrWords; ++w) {
+    volatile unsigned* p = L.err_host + w;
+    if (*p) bits |= 1u << w, *p = 0;
+  }
+  return bits;
+}
+
+void raise_errors(uint32_t bits) {
+  if (!bits) return;
+  std::string m = "FSEP layer step failed on the device:";
+  if (bits & (1u << kErrRecvOverflow)) m += " receive buffer overflow (max_recv_rows too small; segments dropped);";
+  if (bits & (1u << kErrBarrierTimeout)) m += " peer barrier timed out (a rank did not arrive);";
+  if (bits & (1u << kErrRestoreTimeout)) m += " restored expert chunk never arrived (readiness flag timeout);";
+  throw Error(ErrorKind::device, m);
+}
+
+void poll_errors(Layer& L) { raise_errors(take_errors(L)); }
 
 bool is_device_ptr(const void* p) {
   cudaPointerAttributes a{};
@@ -789,8 +836,19 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     require(static_cast<long long>(d.max_tokens) * d.top_k < (1LL << kRowSrcShift), "max_tokens * top_k must stay below 2^26");
     // copy-engine communication for real multi-GPU mode (FSEP_COMM=kernel selects the SM kernels);
     // decided before carving the arena (push targets live in it; identical on every rank)
+    // Virtual mode runs the same copy-engine transport between the emulated ranks with
+    // MP_FSEP_FLAG_COPY_ENGINE (or FSEP_COMM=ce), so one GPU exercises the shipped N>1 path.
     const char* comm = std::getenv("FSEP_COMM");
-    L->ce_mode = !L->virt && L->N > 1 && !(comm && std::string(comm) == "kernel") && write_value_fn() != nullptr;
+    const bool want_ce = L->virt ? ((d.flags & MP_FSEP_FLAG_COPY_ENGINE) != 0 || (comm && std::string(comm) == "ce"))
+                                 : !(comm && std::string(comm) == "kernel");
+    L->ce_mode = L->N > 1 && want_ce && write_value_fn() != nullptr;
+    require(!(L->virt && (d.flags & MP_FSEP_FLAG_COPY_ENGINE)) || L->ce_mode || L->N == 1,
+            "copy-engine mode unavailable (cuStreamWriteValue32 entry point missing)");
+    if (const char* v = std::getenv("FSEP_SPIN_TIMEOUT_MS"))
+      L->spin_timeout_ns = static_cast<unsigned long long>(std::max(1.0, std::atof(v)) * 1e6);
+    CK(cudaHostAlloc(&L->err_host, kErrWords * sizeof(unsigned), cudaHostAllocMapped));
+    std::memset(L->err_host, 0, kErrWords * sizeof(unsigned));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&L->err_dev), L->err_host, 0));
     const int local = L->virt ? L->N : 1;
     L->ranks.resize(local);
     for (int v = 0; v < local; ++v) {
@@ -859,6 +917,7 @@ void mp_fsep_layer_free(mp_fsep_layer* L) {
   cudaStreamDestroy(L->side);
   cudaStreamDestroy(L->plan_stream);
   cudaStreamDestroy(L->cap_stream);
+  cudaFreeHost(L->err_host);
   if (L->ce_mode) {
     for (int p = 0; p < L->N; ++p) {
       cudaStreamDestroy(L->ce[p]);
@@ -872,6 +931,8 @@ void mp_fsep_layer_free(mp_fsep_layer* L) {
   for (auto& ring : L->ev_g)
     for (auto e : ring) cudaEventDestroy(e);
   for (auto& ring : L->ev_p)
+    for (auto e : ring) cudaEventDestroy(e);
+  for (auto& ring : L->ev_ce_t)
     for (auto e : ring) cudaEventDestroy(e);
   delete L;
 }
@@ -1026,6 +1087,7 @@ mp_status mp_fsep_layer_forward(mp_fsep_layer* L, const void* x, const float* bi
     require(L && x && y, "mp_fsep_layer_forward: NULL argument");
     require(L->connected, "mp_fsep_layer_forward: multi-GPU layer not connected");
     CK(cudaSetDevice(L->device));
+    poll_errors(*L);
     L->launches_before = launches_issued();
     run_forward(*L, static_cast<const __nv_bfloat16*>(x), bias, static_cast<int>(n_tokens),
                 static_cast<__nv_bfloat16*>(y), static_cast<cudaStream_t>(stream));
@@ -1037,6 +1099,7 @@ mp_status mp_fsep_layer_backward(mp_fsep_layer* L, const void* dy, void* dx, voi
   return guarded([&] {
     require(L && dy && dx, "mp_fsep_layer_backward: NULL argument");
     CK(cudaSetDevice(L->device));
+    poll_errors(*L);
     run_backward(*L, static_cast<const __nv_bfloat16*>(dy), static_cast<__nv_bfloat16*>(dx),
                  static_cast<cudaStream_t>(stream));
     L->launches_step = launches_issued() - L->launches_before;
@@ -1156,6 +1219,37 @@ mp_status mp_fsep_layer_stats(mp_fsep_layer* L, uint64_t* kernel_launches, doubl
       }
       *gemm_flops = 18.0 * L->H * L->F * static_cast<double>(rows);
     }
+    poll_errors(*L);  // the step whose numbers these are must not have failed
+  });
+}
+
+mp_status mp_fsep_layer_check(mp_fsep_layer* L, uint32_t* bits) {
+  if (bits) *bits = 0;
+  return guarded([&] {
+    require(L, "mp_fsep_layer_check: NULL layer");
+    CK(cudaSetDevice(L->device));
+    CK(cudaDeviceSynchronize());
+    const uint32_t b = take_errors(*L);
+    if (bits) *bits = b;
+    raise_errors(b);
+  });
+}
+
+mp_status mp_fsep_layer_debug_inject(mp_fsep_layer* L, const char* what) {
+  return guarded([&] {
+    require(L && what, "mp_fsep_layer_debug_inject: NULL argument");
+    CK(cudaSetDevice(L->device));
+    const std::string w(what);
+    if (w == "drop_restore_flag") {
+      require(L->ce_mode, "drop_restore_flag needs copy-engine mode");
+      L->drop_flag = L->virt ? 1 : L->ranks[0].rank;  // virtual: emulated rank 1's push to a peer
+    } else if (w == "barrier_timeout") {
+      require(L->virt && L->N > 1, "barrier_timeout is emulated in virtual mode (rank 0 waits alone)");
+      launch_peer_barrier(L->d_peer_flags, L->N, 0, L->epoch + 0x40000000u, L->err_dev, L->spin_timeout_ns, nullptr);
+      CK(cudaDeviceSynchronize());
+    } else {
+      throw Error(ErrorKind::invalid_argument, "mp_fsep_layer_debug_inject: unknown condition " + w);
+    }
   });
 }
 
@@ -1252,6 +1346,7 @@ mp_status mp_fsep_layer_graph_step(mp_fsep_layer* L, const void* x, const float*
     require(L && x && y && dy && dx, "mp_fsep_layer_graph_step: NULL argument");
     auto st = static_cast<cudaStream_t>(stream);
     CK(cudaSetDevice(L->device));
+    poll_errors(*L);
     const void* key[5] = {x, bias, y, dy, dx};
     const bool same = L->graph && std::memcmp(key, L->graph_key, sizeof(key)) == 0 && L->T_step == static_cast<int>(n_tokens);
     if (!same) {

@@ -38,6 +38,7 @@ class LayerSpec:
     max_recv_rows: int = 0
     resident: bool = False  # MP_FSEP_FLAG_RESIDENT_EXPERTS: pure EP baseline (E == N*C, fixed layout)
     local_first: bool = False  # MP_FSEP_FLAG_LOCAL_FIRST: non-parity local-first token routing
+    copy_engine: bool = False  # MP_FSEP_FLAG_COPY_ENGINE: virtual mode runs the real N>1 copy-engine transport
 
 
 def _stream(stream=None):
@@ -61,7 +62,8 @@ class FsepLayer:
         self.device = torch.cuda.current_device() if device is None else device
         d = FsepDesc(spec.n_experts, spec.top_k, spec.hidden, spec.ffn, spec.max_tokens, spec.capacity, spec.world,
                      spec.rank, 1 if spec.virtual else 0,
-                     (1 if spec.resident else 0) | (2 if spec.local_first else 0), spec.max_recv_rows)
+                     (1 if spec.resident else 0) | (2 if spec.local_first else 0) | (4 if spec.copy_engine else 0),
+                     spec.max_recv_rows)
         h = C.c_void_p()
         check(self.lib.mp_fsep_layer_create(C.byref(d), self.device, C.byref(h)))
         self._h = h
@@ -108,7 +110,7 @@ class FsepLayer:
         return self._planner
 
     def chain(self, next_layer: Optional["FsepLayer"]) -> None:
-        """Issue next_layer's shard restore after this layer's dispatch (PAPER Fig.5)."""
+        """Issue next_layer's shard restore after this layer's gate-up GEMM (PAPER Fig.5)."""
         check(self.lib.mp_fsep_layer_chain(self._h, next_layer._h if next_layer is not None else None))
 
     def detach_planner(self) -> None:
@@ -174,6 +176,18 @@ class FsepLayer:
         if self.lib.mp_fsep_layer_phase_ms(self._h, out, len(self.PHASES)) != 0:
             return None
         return {k: round(out[i], 4) for i, k in enumerate(self.PHASES)}
+
+    def check(self) -> int:
+        """Synchronise and report device-detected failures of the steps so far
+        (raises MoeplanError, status MP_ERR_DEVICE, if any; returns 0 otherwise)."""
+        bits = C.c_uint32()
+        st = self.lib.mp_fsep_layer_check(self._h, C.byref(bits))
+        self.last_error_bits = bits.value
+        check(st)
+        return bits.value
+
+    def debug_inject(self, what: str) -> None:
+        check(self.lib.mp_fsep_layer_debug_inject(self._h, what.encode()))
 
     def stats_reset(self) -> None:
         check(self.lib.mp_fsep_layer_stats_reset(self._h))

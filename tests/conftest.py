@@ -6,6 +6,7 @@ import pytest
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))  # shared helpers (torch_ref, test_gpu_layer)
 
 
 def pytest_configure(config):

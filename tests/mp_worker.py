@@ -63,6 +63,7 @@ def main():
                  R=layer.histogram(), dwg=layer.router_grad().cpu().numpy(),
                  dw1=dw[0].cpu().numpy(), dw3=dw[1].cpu().numpy(), dw2=dw[2].cpu().numpy(),
                  barrier=layer.read("barrier_status").view(np.uint32))
+    assert layer.check() == 0  # no barrier / readiness timeout, no receive overflow
     if rank == 0:
         np.savez(out_dir / "weights.npz", wg=wg.float().numpy(), w1=w1.float().numpy(), w3=w3.float().numpy(),
                  w2=w2.float().numpy())

@@ -2,7 +2,7 @@
 one process per GPU, copy-engine communication).  Checks, in real multi-GPU mode:
 
 * layer chaining (mp_fsep_layer_chain, PAPER Fig.5): a 2-layer step with layer 2's
-  restore issued after layer 1's dispatch gives bit-identical outputs and
+  restore issued after layer 1's gate-up GEMM gives bit-identical outputs and
   gradients to the unchained step;
 * pure-EP resident experts (MP_FSEP_FLAG_RESIDENT_EXPERTS): y / dx match the CPU
   oracle on the static layout, and a second step (no restore) reproduces the

@@ -113,3 +113,29 @@ def test_wgrad(counts, M, N, pair):
         else:
             assert _rel(out[g], ref) < 1e-3
         o += c
+
+
+# Production-schedule wgrad launches: many tiles over several waves of the 74 CTA
+# pairs.  (a) Zipf-skewed group rows: longest-processing-time group order and snake
+# wave assignment (grouped_gemm2.cuh wave_tile); (b) >= 2 x 148 tiles per group, which
+# turns on the wave-synchronised producers (wave_barrier) as for the Mixtral dW13.
+@pytest.mark.parametrize("counts,M,N", [
+    ([4096, 1920, 1152, 768, 640, 512, 384, 256, 256, 128, 128, 128, 0, 128, 384, 0], 1024, 1408),
+    ([512, 1024], 8192, 2560),
+], ids=["zipf_lpt_snake_5waves", "wave_sync_4waves"])
+def test_wgrad_multiwave(counts, M, N):
+    torch.manual_seed(2)
+    G = len(counts)
+    rows, off, R = _groups(counts)
+    A = torch.randn(R, M, device="cuda").bfloat16()
+    B = torch.randn(R, N, device="cuda").bfloat16()
+    out = torch.full((G, M, N), float("nan"), device="cuda")
+    _run("wgrad", G, rows, off, M, N, 0, A, R, M, B, N, R, 1, N, 0, out, N, ogs=M * N, pair=True)
+    o = 0
+    for g, c in enumerate(counts):
+        if c == 0:
+            assert (out[g] == 0).all()
+        else:
+            ref = A[o:o + c].float().t() @ B[o:o + c].float()
+            assert _rel(out[g], ref) < 1e-3, g
+        o += c

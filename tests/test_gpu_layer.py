@@ -39,8 +39,9 @@ def make_problem(N, E, K, H, F, T, alpha, seed):
     return dict(wg=wg, w1=w1, w3=w3, w2=w2, xs=xs, dys=dys, biases=biases)
 
 
-def run_gpu(pb, N, E, K, H, F, T, C, A, virtual=True, resident=False, local_first=False):
-    spec = LayerSpec(E, K, H, F, T, C, world=N, virtual=virtual, resident=resident, local_first=local_first)
+def run_gpu(pb, N, E, K, H, F, T, C, A, virtual=True, resident=False, local_first=False, copy_engine=False):
+    spec = LayerSpec(E, K, H, F, T, C, world=N, virtual=virtual, resident=resident, local_first=local_first,
+                     copy_engine=copy_engine)
     layer = FsepLayer(spec)
     for e in range(E):
         layer.load_expert(e, pb["w1"][e].cuda().contiguous(), pb["w3"][e].cuda().contiguous(),
