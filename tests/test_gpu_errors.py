@@ -52,21 +52,22 @@ def _expect_device_error(layer, bit, text):
 def test_receive_overflow_is_reported():
     N, E, K, H, F, T, C = 4, 8, 2, 256, 256, 256, 2
     layer, io = _layer(N, E, K, H, F, T, C, max_recv_rows=128)
-    _step(layer, io)
+    layer.forward(io["x"], io["bias"], io["T"], io["y"])
     _expect_device_error(layer, 0, "receive buffer overflow")
     assert layer.read("status", 0).view(np.int32)[0] == 1 or any(
         layer.read("status", v).view(np.int32)[0] == 1 for v in range(N))
     layer.close()
 
 
-def test_overflow_reported_by_next_forward():
+def test_overflow_reported_by_next_call():
     N, E, K, H, F, T, C = 4, 8, 2, 256, 256, 256, 2
     layer, io = _layer(N, E, K, H, F, T, C, max_recv_rows=128)
-    _step(layer, io)
+    layer.forward(io["x"], io["bias"], io["T"], io["y"])
     torch.cuda.synchronize()
-    with pytest.raises(MoeplanError) as ei:
-        layer.forward(io["x"], io["bias"], io["T"], io["y"])
+    with pytest.raises(MoeplanError) as ei:  # the step's own backward already sees it
+        layer.backward(io["dy"], io["dx"])
     assert ei.value.status == MP_ERR_DEVICE
+    assert layer.check() == 0  # reported once
     layer.close()
 
 

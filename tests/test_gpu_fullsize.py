@@ -77,5 +77,7 @@ def test_full_size_parity(E, K, H, F, T):
     errs["dx"] = _rel(dx, dxs[0])
     errs["dWg"] = _rel(layer.router_grad(0), dWgs[0])
     worst = max(errs, key=errs.get)
+    print(f"\nfull-size parity {E}x{H}x{F}: worst {worst} {errs[worst]:.3e}; y {errs['y']:.3e} dx {errs['dx']:.3e} "
+          f"dWg {errs['dWg']:.3e}")
     assert errs[worst] < TOL, f"{worst}: {errs[worst]:.3e}  (all: {errs})"
     layer.close()
