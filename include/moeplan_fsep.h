@@ -126,6 +126,15 @@ typedef struct mp_fsep_desc {
  * reduce-scatter kernels.  This is how one GPU checks the shipped N>1 data plane
  * against the oracle (real mode always uses it unless FSEP_COMM=kernel). */
 #define MP_FSEP_FLAG_COPY_ENGINE 4u
+/* Gradient-communication delay (PAPER Fig.5(e)): for a layer with a
+ * chained predecessor (mp_fsep_layer_chain(prev, layer)), the owner-side half of
+ * this layer's gradient reduce-scatter -- waiting for the replicas' pushed chunks,
+ * the cross-rank barrier and the ascending-device sum -- is not run at the end of
+ * this layer's backward but on a side stream under the predecessor's backward
+ * GEMMs (the next expert layer in backward order).  Copy-engine mode only.  The
+ * gradients are final once the predecessor's backward has run, or on the stream
+ * passed to mp_fsep_layer_expert_grad (which completes a still-pending deferral). */
+#define MP_FSEP_FLAG_DEFER_RS 8u
 
 mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_layer** out);
 void mp_fsep_layer_free(mp_fsep_layer* layer);

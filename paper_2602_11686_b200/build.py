@@ -45,7 +45,13 @@ def _cuda_home() -> Path:
 
 
 def lib_path() -> Path:
-    return LIBDIR / LIBNAME
+    # FSEP_LIB_NAME selects a dev variant (e.g. a -DFSEP_GEMM_STALLS build, with its own objects)
+    return LIBDIR / os.environ.get("FSEP_LIB_NAME", LIBNAME)
+
+
+def _objdir() -> Path:
+    v = os.environ.get("FSEP_LIB_NAME")
+    return OBJDIR if not v else LIBDIR / ("obj_" + v.replace(".so", ""))
 
 
 def _headers_mtime() -> float:
@@ -71,7 +77,8 @@ def _run(cmd):
 
 
 def build(verbose: bool = False, force: bool = False, jobs: int | None = None) -> Path:
-    OBJDIR.mkdir(parents=True, exist_ok=True)
+    objdir = _objdir()
+    objdir.mkdir(parents=True, exist_ok=True)
     host, cuda = _sources()
     hdr_t = _headers_mtime()
     inc = ["-I", str(ROOT / "include"), "-I", str(CSRC), "-I", str(_json_dir()),
@@ -84,7 +91,7 @@ def build(verbose: bool = False, force: bool = False, jobs: int | None = None) -
     jobs_ = []
     objs = []
     for src in host + cuda:
-        obj = OBJDIR / (src.stem + (".cu.o" if src.suffix == ".cu" else ".o"))
+        obj = objdir / (src.stem + (".cu.o" if src.suffix == ".cu" else ".o"))
         objs.append(obj)
         if not force and obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_t):
             continue

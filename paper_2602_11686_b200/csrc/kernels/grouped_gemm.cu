@@ -38,6 +38,21 @@ void check_encode(CUresult r, const char* what) {
 }  // namespace
 
 uint64_t launches_issued() { return g_launches.load(); }
+
+bool gemm_stall_counters(unsigned long long* out, bool reset) {
+#ifdef FSEP_GEMM_STALLS
+  if (cudaMemcpyFromSymbol(out, g_gemm_stall, sizeof(g_gemm_stall)) != cudaSuccess) return false;
+  if (reset) {
+    const unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_gemm_stall, z, sizeof(z));
+  }
+  return true;
+#else
+  (void)out;
+  (void)reset;
+  return false;
+#endif
+}
 // Every launcher calls this right after its launch: count it, and surface launch
 // errors (bad configuration, shared-memory limits) at the call that caused them.
 void count_launch(int n) {
@@ -152,7 +167,7 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
     return v ? std::atoi(v) : 0;
   }();
   if (kind == GemmKind::kBwdWgrad && p.raster == 0) p.raster = wgrad_raster;
-  if (wave_sync && a.wave_sync != nullptr && long_k) {
+  if (wave_sync && a.wave_sync != nullptr && long_k && !(a.policy & 0x800)) {  // policy bit 11: A/B off
     cudaMemsetAsync(a.wave_sync, 0, kWaveSyncMax * sizeof(int), stream);
     p.wave_sync = a.wave_sync;
   }

@@ -25,6 +25,20 @@
 
 namespace fsep {
 
+#ifdef FSEP_GEMM_STALLS
+// Stall accounting (dev builds, -DFSEP_GEMM_STALLS): cycles each role spends in its
+// barrier waits, summed over CTAs: [0] MMA waits for operands (full), [1] MMA waits
+// for a free accumulator (tempty), [2] producer waits for a free stage (empty),
+// [3] epilogue waits for an accumulator (tfull), [4] MMA-warp lifetime,
+// [5] epilogue busy (drain) cycles, [6] producer readiness + wave-barrier waits.
+__device__ unsigned long long g_gemm_stall[8];
+#define FSEP_STALL_T0() const long long _t0 = clock64()
+#define FSEP_STALL_ADD(acc) (acc) += clock64() - _t0
+#else
+#define FSEP_STALL_T0()
+#define FSEP_STALL_ADD(acc)
+#endif
+
 namespace gemm2 {
 constexpr int BM = 256, BN = 256, BK = 64, STAGES = 6;
 constexpr int HALF = 128;                       // rows of A / columns of B per CTA
@@ -224,16 +238,23 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
       int ready_g = -1;
       bool ready_live = true;
       bool wsync = p.wave_sync != nullptr;
+      long long st_empty = 0, st_sync = 0;
       for (int w = 0, t = wave_tile(0); t < total_tiles; t = wave_tile(++w)) {
-        if (wsync && w > 0 && w <= kWaveSyncMax)  // CTAs with a tile in wave w
-          wsync = wave_barrier(p.wave_sync + (w - 1), 2 * min(nclusters, total_tiles - w * nclusters));
+        {
+          FSEP_STALL_T0();
+          if (wsync && w > 0 && w <= kWaveSyncMax)  // CTAs with a tile in wave w
+            wsync = wave_barrier(p.wave_sync + (w - 1), 2 * min(nclusters, total_tiles - w * nclusters));
+          FSEP_STALL_ADD(st_sync);
+        }
         int g, mb, nbk;
         decode(t, g, mb, nbk);
         const int nk = k_blocks(g);
         const int row0 = p.group_off[g];
         if (!kGroupK && g != ready_g && ready_live) {
+          FSEP_STALL_T0();
           ready_live = wait_group_ready(p, g);  // false: timed out (error raised), stop waiting
           ready_g = g;
+          FSEP_STALL_ADD(st_sync);
         }
         const int m_half = mb * BM + rank * HALF;   // this CTA's first A row (M-grouped: within the group)
         // this CTA's first B column; a last N tile with <= 128 live columns runs as
@@ -241,7 +262,11 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
         const bool n_tail = p.N - nbk * BN <= HALF && !(p.policy & 0x100);
         const int n_half = nbk * BN + rank * (n_tail ? HALF / 2 : HALF);
         for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&empty_bar[s], ph ^ 1);
+          {
+            FSEP_STALL_T0();
+            mbar_wait(&empty_bar[s], ph ^ 1);
+            FSEP_STALL_ADD(st_empty);
+          }
           uint8_t* sA = smem + s * STAGE_BYTES;
           uint8_t* sB = sA + A_BYTES;
           if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * STAGE_BYTES);
@@ -271,6 +296,10 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
           }
         }
       }
+#ifdef FSEP_GEMM_STALLS
+      atomicAdd(&g_gemm_stall[2], static_cast<unsigned long long>(st_empty));
+      atomicAdd(&g_gemm_stall[6], static_cast<unsigned long long>(st_sync));
+#endif
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader CTA)
@@ -280,18 +309,30 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
+      long long st_full = 0, st_tempty = 0;
+#ifdef FSEP_GEMM_STALLS
+      const long long t_begin = clock64();
+#endif
       for (int w = 0, t = wave_tile(0); t < total_tiles; t = wave_tile(++w), ++it) {
         int g, mb, nbk;
         decode(t, g, mb, nbk);
         const int nk = k_blocks(g);
         const int as = it & 1;
         const uint32_t aph = (it >> 1) & 1;
-        mbar_wait(&tempty_bar[as], aph ^ 1);
+        {
+          FSEP_STALL_T0();
+          mbar_wait(&tempty_bar[as], aph ^ 1);
+          FSEP_STALL_ADD(st_tempty);
+        }
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + as * BN;
         const uint32_t id = (p.N - nbk * BN <= HALF && !(p.policy & 0x100)) ? idesc_tail : idesc;
         for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&full_bar[s], ph);
+          {
+            FSEP_STALL_T0();
+            mbar_wait(&full_bar[s], ph);
+            FSEP_STALL_ADD(st_full);
+          }
           tc_fence_after();
           if (lane == 0) {
             const uint32_t a0 = smem_u32(smem + s * STAGE_BYTES);
@@ -314,6 +355,13 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
         if (lane == 0) umma_commit_pair(&tfull_bar[as], 0x3);
         __syncwarp();
       }
+#ifdef FSEP_GEMM_STALLS
+      if (lane == 0) {
+        atomicAdd(&g_gemm_stall[0], static_cast<unsigned long long>(st_full));
+        atomicAdd(&g_gemm_stall[1], static_cast<unsigned long long>(st_tempty));
+        atomicAdd(&g_gemm_stall[4], static_cast<unsigned long long>(clock64() - t_begin));
+      }
+#endif
     }
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
@@ -321,6 +369,7 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
     const int half0 = NHALF == 1 ? static_cast<int>(warp - 2) >> 2 : 0;
     const int r = static_cast<int>(quarter * 32 + lane);  // row within this CTA's 128 rows
     int it = 0;
+    long long st_tfull = 0, st_drain = 0;
     for (int w = 0, t = wave_tile(0); t < total_tiles; t = wave_tile(++w), ++it) {
       int g, mb, nbk;
       decode(t, g, mb, nbk);
@@ -340,7 +389,14 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
           }
         }
       }
-      mbar_wait(&tfull_bar[as], aph);
+      {
+        FSEP_STALL_T0();
+        mbar_wait(&tfull_bar[as], aph);
+        FSEP_STALL_ADD(st_tfull);
+      }
+#ifdef FSEP_GEMM_STALLS
+      const long long t_drain = clock64();
+#endif
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((quarter * 32) << 16) + as * BN;
       if (valid)
@@ -514,6 +570,9 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
           }
         }
       }
+#ifdef FSEP_GEMM_STALLS
+      st_drain += clock64() - t_drain;
+#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -523,6 +582,12 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
           mbar_arrive_remote(&tempty_bar[as], 0);
       }
     }
+#ifdef FSEP_GEMM_STALLS
+    if (lane == 0) {
+      atomicAdd(&g_gemm_stall[3], static_cast<unsigned long long>(st_tfull));
+      atomicAdd(&g_gemm_stall[5], static_cast<unsigned long long>(st_drain));
+    }
+#endif
   }
   __syncthreads();
   tc_fence_before();

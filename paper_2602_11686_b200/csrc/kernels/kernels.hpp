@@ -61,6 +61,9 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
 
 // Kernel-count bookkeeping for bench/roofline (launches issued by this library).
 uint64_t launches_issued();
+// Dev builds (-DFSEP_GEMM_STALLS): per-role barrier-wait cycle totals of the pair
+// GEMM (grouped_gemm2.cuh g_gemm_stall); false when compiled out.
+bool gemm_stall_counters(unsigned long long* out8, bool reset);
 void count_launch(int n = 1);
 
 }  // namespace fsep

@@ -35,7 +35,8 @@ __attribute__((visibility("default"))) mp_status mp_fsep_debug_grouped_gemm(
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     GroupedGemmArgs g{num_groups, group_rows, group_off, M, N, K, out, ldo, out_gstride, out2, ldo2, aux, ld_aux};
-    g.policy = (kind >> 12) & 0xF;   // experiment knobs (bits 12-15 policy, 16-23 raster)
+    // experiment knobs: bits 12-15 L2 policy, 16-23 raster, 24-27 GemmParams::policy bits 8-11
+    g.policy = ((kind >> 12) & 0xF) | (((kind >> 24) & 0xF) << 8);
     g.raster = (kind >> 16) & 0xFF;
     static int* wave_sync = nullptr;  // wave-synchronisation counters, as the layer step passes them
     if (wave_sync == nullptr && cudaMalloc(&wave_sync, kWaveSyncMax * sizeof(int)) != cudaSuccess)
@@ -47,6 +48,14 @@ __attribute__((visibility("default"))) mp_status mp_fsep_debug_grouped_gemm(
       launch_grouped_gemm(k, ta, tb, g, sms, static_cast<cudaStream_t>(stream));
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw moeplan::Error(moeplan::ErrorKind::device, cudaGetErrorString(e));
+  });
+}
+
+// Dev builds only (-DFSEP_GEMM_STALLS via FSEP_NVCC_EXTRA): role wait-cycle totals.
+__attribute__((visibility("default"))) mp_status mp_fsep_debug_gemm_stalls(unsigned long long* out8, int reset) {
+  return moeplan::capi::guarded([&] {
+    if (!fsep::gemm_stall_counters(out8, reset != 0))
+      throw moeplan::Error(moeplan::ErrorKind::invalid_argument, "built without FSEP_GEMM_STALLS");
   });
 }
 

@@ -82,6 +82,7 @@ struct Rank {
   float* grad_full = nullptr;
   __nv_bfloat16* shard = nullptr;
   unsigned int* flags = nullptr;
+  unsigned int* rs_flags = nullptr;  // [N+1] barrier flags of the deferred reduce-scatter (side stream)
   unsigned* ready = nullptr;   // [kMaxExperts][kMaxRanks] restore readiness (written by the pushing peers)
   float* rs_stage = nullptr;   // [E][N][S] replica grad chunks pushed by the hosts (owner side)
   // private
@@ -145,6 +146,15 @@ extern "C" struct mp_fsep_layer {
   bool local_first = false;    // MP_FSEP_FLAG_LOCAL_FIRST (non-parity routing variant)
   bool dedupe = false;         // token rows cross NVLink once per destination device (K >= 4)
   mp_fsep_layer* next = nullptr;  // chained next layer: its restore is issued after this layer's gate-up GEMM
+  mp_fsep_layer* prev = nullptr;  // chained previous layer: its backward completes our deferred reduce-scatter
+  // Fig.5(e) gradient-communication delay (MP_FSEP_FLAG_DEFER_RS): the owner-side half of
+  // the reduce-scatter (wait for the pushes, barrier, ascending-device sum) runs on the
+  // side stream under the previous layer's backward GEMMs instead of ending this backward.
+  bool defer_rs = false;
+  int rs_state = 0;  // 0 done, 1 pushes issued / sum pending, 2 sum enqueued on the side stream (ev_rs_done)
+  unsigned int** d_peer_rs_flags = nullptr;
+  unsigned int rs_epoch = 0;
+  cudaEvent_t ev_rs_done = nullptr;
   bool prefetched = false;        // this layer's restore for the coming forward is already in flight
   bool restore_split = true;      // push slot 0 before dispatch, the rest after (FSEP_RESTORE_SPLIT=0: all before)
   // graph
@@ -284,6 +294,7 @@ void allocate_rank(Layer& L, Rank& r) {
   acc(C * flat * 4);  // grad_full
   acc(E * S * 2);    // shard
   acc((N + 1) * 4);  // flags
+  acc((N + 1) * 4);  // rs_flags
   const bool push = L.ce_mode;
   if (push) {
     acc(C * flat * 2);                      // restored (push target)
@@ -306,6 +317,7 @@ void allocate_rank(Layer& L, Rank& r) {
   r.grad_full = ca.take<float>(C * flat);
   r.shard = ca.take<__nv_bfloat16>(E * S);
   r.flags = ca.take<unsigned int>(N + 1);
+  r.rs_flags = ca.take<unsigned int>(N + 1);
   if (push) {
     r.restored = ca.take<__nv_bfloat16>(C * flat);
     r.ready = ca.take<unsigned>(kMaxExperts * kMaxRanks);
@@ -392,6 +404,29 @@ void finish_peers(Layer& L) {
 void barrier(Layer& L, cudaStream_t st) {
   if (L.virt || L.N == 1) return;  // stream order is the barrier on one GPU
   launch_peer_barrier(L.d_peer_flags, L.N, L.ranks[0].rank, ++L.epoch, L.err_dev, L.spin_timeout_ns, st);
+}
+
+// Owner-side completion of a reduce-scatter whose pushes were issued by L's backward:
+// on L's side stream wait for L's own pushes, then (real mode) a barrier on the
+// separate rs flags (everyone's pushes landed), then the ascending-device sum.
+void finish_rs_async(Layer& L) {
+  if (L.rs_state != 1) return;
+  for (int o = 0; o < L.N; ++o) CK(cudaStreamWaitEvent(L.side, L.ev_ce[o], 0));
+  if (!L.virt && L.N > 1)
+    launch_peer_barrier(L.d_peer_rs_flags, L.N, L.ranks[0].rank, ++L.rs_epoch, L.err_dev, L.spin_timeout_ns, L.side);
+  for (Rank& r : L.ranks)
+    launch_grad_rs_sum(r.pt, r.grad_full, r.rs_stage, L.E, L.N, r.rank, L.S, L.flat, r.grad_shard, L.side);
+  CK(cudaEventRecord(L.ev_rs_done, L.side));
+  L.rs_state = 2;
+}
+
+// Make L's reduced gradient shards final on `st` (finishing a still-pending deferral).
+void join_rs(Layer& L, cudaStream_t st) {
+  finish_rs_async(L);
+  if (L.rs_state == 2) {
+    CK(cudaStreamWaitEvent(st, L.ev_rs_done, 0));
+    L.rs_state = 0;
+  }
 }
 
 // CTA-pair (cta_group::2) kernel by default; FSEP_GEMM=single forces the 128x256 single-CTA kernel.
@@ -629,6 +664,14 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
 void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStream_t st) {
   const int E = L.E, K = L.K, H = L.H, F = L.F, N = L.N, T = L.T_step;
   const long long TH = static_cast<long long>(T) * H;
+  // Fig.5(e): the next layer (already back-propagated this step) deferred the owner-side
+  // half of its reduce-scatter; it runs on that layer's side stream under this layer's GEMMs.
+  Layer* deferred = (L.next && L.next->rs_state == 1) ? L.next : nullptr;
+  if (deferred) {
+    CK(cudaEventRecord(L.ev_fork, st));
+    CK(cudaStreamWaitEvent(deferred->side, L.ev_fork, 0));
+    finish_rs_async(*deferred);
+  }
   for (size_t v = 0; v < L.ranks.size(); ++v) {
     Rank& r = L.ranks[v];
     launch_combine_bwd(T, H, K, dy + (L.virt ? static_cast<long long>(v) * TH : 0), r.topk_w, r.topk_idx, r.tok_rows,
@@ -647,6 +690,8 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   // on the copy engines underneath the GEMMs that follow.
   const bool rs = N > 1 && !L.resident;  // pure EP: gradients stay whole on their single host
   const bool ce_rs = L.ce_mode && rs;
+  // the previous chained layer's backward (run next) completes the reduce-scatter
+  const bool defer = ce_rs && L.defer_rs && L.prev != nullptr;
   // Push this rank's replica-gradient chunks [lo, hi) of the flat vector to their
   // owners' staging rows (copy engines, one stream per owner), after `ev`.
   auto push_grads = [&](cudaEvent_t ev, long long lo, long long hi) {
@@ -717,7 +762,12 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   }
   CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][3], st));
   mark(L, st, kPhBwdGemm);
-  if (ce_rs) {
+  if (defer) {
+    mark(L, st, kPhRsPushWait);
+    barrier(L, st);  // every rank's dX GEMM stored its dX rows into our tok_rows
+    mark(L, st, kPhRsBarrier);
+    L.rs_state = 1;
+  } else if (ce_rs) {
     for (int o = 0; o < N; ++o) CK(cudaStreamWaitEvent(st, L.ev_ce[o], 0));  // own pushes landed
     mark(L, st, kPhRsPushWait);
     // ... and everyone else's: this barrier also orders every rank's dX GEMM (whose
@@ -741,6 +791,7 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   if (rs && !ce_rs)
     for (Rank& r : L.ranks) launch_grad_reduce_scatter(r.pt, L.peers, E, r.rank, L.S, L.flat, r.grad_shard, st);
   mark(L, st, kPhGradRS);
+  if (deferred) join_rs(*deferred, st);  // long finished under this layer's GEMMs
   // join the planner stream (it finished long before the backward GEMMs did)
   if (L.planner_pending) CK(cudaStreamWaitEvent(st, L.ev_planned, 0));
 }
@@ -823,6 +874,7 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     L->virt = d.virtual_ranks != 0 || L->N == 1;
     L->resident = (d.flags & MP_FSEP_FLAG_RESIDENT_EXPERTS) != 0;
     L->local_first = (d.flags & MP_FSEP_FLAG_LOCAL_FIRST) != 0;
+    L->defer_rs = (d.flags & MP_FSEP_FLAG_DEFER_RS) != 0;
     // de-duplicated token transfers pay off when a token has several slots per
     // device (top-k >= 4); FSEP_DEDUPE=0/1 overrides
     L->dedupe = L->N > 1 && d.top_k >= 4 && use_tma_dispatch();
@@ -864,7 +916,7 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     CK(cudaStreamCreateWithFlags(&L->side, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&L->plan_stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&L->cap_stream, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&L->ev_fork, &L->ev_restored, &L->ev_hist, &L->ev_planned})
+    for (cudaEvent_t* e : {&L->ev_fork, &L->ev_restored, &L->ev_hist, &L->ev_planned, &L->ev_rs_done})
       CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     for (auto& ring : L->ev_g)
       for (auto& e : ring) CK(cudaEventCreate(&e));
@@ -888,6 +940,7 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
       CK(cudaMallocHost(&L->layout_ring, 4 * static_cast<size_t>(L->E) * L->N));
     }
     CK(cudaMalloc(&L->d_peer_flags, sizeof(unsigned int*) * kMaxRanks));
+    CK(cudaMalloc(&L->d_peer_rs_flags, sizeof(unsigned int*) * kMaxRanks));
     CK(cudaMalloc(&L->d_tok_table, sizeof(__nv_bfloat16*) * kMaxRanks));
     if (L->virt) {
       unsigned int* f[kMaxRanks] = {};
@@ -903,6 +956,8 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
 void mp_fsep_layer_free(mp_fsep_layer* L) {
   if (!L) return;
   cudaSetDevice(L->device);
+  if (L->prev && L->prev->next == L) L->prev->next = nullptr;
+  if (L->next && L->next->prev == L) L->next->prev = nullptr;
   cudaDeviceSynchronize();
   if (L->graph) cudaGraphExecDestroy(L->graph);
   for (void* p : L->opened_ptrs) cudaIpcCloseMemHandle(p);
@@ -911,6 +966,7 @@ void mp_fsep_layer_free(mp_fsep_layer* L) {
     cudaFree(r.priv);
   }
   cudaFree(L->d_peer_flags);
+  cudaFree(L->d_peer_rs_flags);
   cudaFree(L->d_tok_table);
   cudaFreeHost(L->layout_host);
   cudaFreeHost(L->R_host);
@@ -927,7 +983,7 @@ void mp_fsep_layer_free(mp_fsep_layer* L) {
     cudaEventDestroy(L->ev_w2);
     cudaFreeHost(L->layout_ring);
   }
-  for (cudaEvent_t e : {L->ev_fork, L->ev_restored, L->ev_hist, L->ev_planned}) cudaEventDestroy(e);
+  for (cudaEvent_t e : {L->ev_fork, L->ev_restored, L->ev_hist, L->ev_planned, L->ev_rs_done}) cudaEventDestroy(e);
   for (auto& ring : L->ev_g)
     for (auto e : ring) cudaEventDestroy(e);
   for (auto& ring : L->ev_p)
@@ -966,6 +1022,7 @@ mp_status mp_fsep_layer_connect(mp_fsep_layer* L, const void* all_handles, const
     const auto* hs = static_cast<const cudaIpcMemHandle_t*>(all_handles);
     Rank& me = L->ranks[0];
     unsigned int* flags[kMaxRanks] = {};
+    unsigned int* rs_flags[kMaxRanks] = {};
     for (int p = 0; p < L->N; ++p) {
       char* base;
       if (p == me.rank) {
@@ -995,8 +1052,10 @@ mp_status mp_fsep_layer_connect(mp_fsep_layer* L, const void* all_handles, const
       L->peers.grad_full[p] = reinterpret_cast<float*>(base + off(me.grad_full));
       L->peers.shard[p] = reinterpret_cast<const __nv_bfloat16*>(base + off(me.shard));
       flags[p] = reinterpret_cast<unsigned int*>(base + off(me.flags));
+      rs_flags[p] = reinterpret_cast<unsigned int*>(base + off(me.rs_flags));
     }
     CK(cudaMemcpy(L->d_peer_flags, flags, sizeof(flags), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(L->d_peer_rs_flags, rs_flags, sizeof(rs_flags), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(L->d_tok_table, L->peers.tok_rows, sizeof(L->peers.tok_rows), cudaMemcpyHostToDevice));
     L->connected = true;
   });
@@ -1067,7 +1126,12 @@ mp_status mp_fsep_layer_chain(mp_fsep_layer* L, mp_fsep_layer* next) {
     require(L, "mp_fsep_layer_chain: NULL layer");
     require(next != L, "mp_fsep_layer_chain: a layer cannot precede itself");
     require(!next || (next->N == L->N && next->device == L->device), "mp_fsep_layer_chain: layers must share devices");
+    if (L->next && L->next->prev == L) {
+      join_rs(*L->next, nullptr);  // nobody completes its deferred reduce-scatter any more
+      L->next->prev = nullptr;
+    }
     L->next = next;
+    if (next) next->prev = L;
   });
 }
 
@@ -1123,6 +1187,7 @@ mp_status mp_fsep_layer_expert_grad(mp_fsep_layer* L, uint32_t expert, float* dw
     require(expert < static_cast<uint32_t>(L->E), "expert out of range");
     require(is_device_ptr(dw1) && is_device_ptr(dw3) && is_device_ptr(dw2), "grad outputs must be device pointers");
     auto st = static_cast<cudaStream_t>(stream);
+    join_rs(*L, st);  // a deferred reduce-scatter not yet completed by the previous layer
     if (L->resident && L->N > 1) {  // whole gradient on the expert's single host
       const uint8_t* A = L->cur_layout ? L->cur_layout : L->layout_host;
       for (Rank& r : L->ranks) {

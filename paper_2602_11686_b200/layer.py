@@ -39,6 +39,7 @@ class LayerSpec:
     resident: bool = False  # MP_FSEP_FLAG_RESIDENT_EXPERTS: pure EP baseline (E == N*C, fixed layout)
     local_first: bool = False  # MP_FSEP_FLAG_LOCAL_FIRST: non-parity local-first token routing
     copy_engine: bool = False  # MP_FSEP_FLAG_COPY_ENGINE: virtual mode runs the real N>1 copy-engine transport
+    defer_rs: bool = False  # MP_FSEP_FLAG_DEFER_RS: reduce-scatter completes under the previous layer's backward
 
 
 def _stream(stream=None):
@@ -62,7 +63,8 @@ class FsepLayer:
         self.device = torch.cuda.current_device() if device is None else device
         d = FsepDesc(spec.n_experts, spec.top_k, spec.hidden, spec.ffn, spec.max_tokens, spec.capacity, spec.world,
                      spec.rank, 1 if spec.virtual else 0,
-                     (1 if spec.resident else 0) | (2 if spec.local_first else 0) | (4 if spec.copy_engine else 0),
+                     (1 if spec.resident else 0) | (2 if spec.local_first else 0) | (4 if spec.copy_engine else 0)
+                     | (8 if spec.defer_rs else 0),
                      spec.max_recv_rows)
         h = C.c_void_p()
         check(self.lib.mp_fsep_layer_create(C.byref(d), self.device, C.byref(h)))

@@ -62,9 +62,28 @@ if os.environ.get("PLAIN") == "1":  # same shapes as the SwiGLU kernels, plain b
     tests["down_dgrad_plain"] = (lambda: _run("up_dgrad", G, rg, off, 0, F, H, dY, R, H, W2, F, H, G, F, H*F, dA, F), 2*R*H*F)
 if os.environ.get("ONLY"):
     tests = {k: v for k, v in tests.items() if k in os.environ["ONLY"].split(",")}
+STALLS = os.environ.get("STALLS") == "1"  # needs FSEP_LIB_NAME=<a -DFSEP_GEMM_STALLS build>
+
+
+def stalls(reset=False):
+    from paper_2602_11686_b200 import _lib
+    out = (C.c_ulonglong * 8)()
+    _lib.check(_lib.load().mp_fsep_debug_gemm_stalls(out, 1 if reset else 0))
+    return list(out)
+
+
 tot_ms = tot_fl = 0
 for name, (fn, fl) in tests.items():
+    if STALLS:
+        torch.cuda.synchronize(); stalls(reset=True)
     ms = bench(fn)
+    if STALLS:
+        torch.cuda.synchronize()
+        c = stalls()
+        life = max(c[4], 1)  # MMA-warp lifetime summed over the leader CTAs
+        print(f"  stalls {name}: mma wait operands {100*c[0]/life:5.1f}%  mma wait accumulator {100*c[1]/life:5.1f}%  "
+              f"producer wait stage {100*c[2]/(2*life):5.1f}%  producer ready/wave {100*c[6]/(2*life):5.1f}%  "
+              f"epilogue wait {100*c[3]/(16*life):5.1f}%  epilogue drain {100*c[5]/(16*life):5.1f}%")
     tot_ms += ms; tot_fl += fl
     eff = fl / (ms * 1e-3) / (148 * 8192 * bench.mhz * 1e6)
     print(f"{name:16s} {ms:8.3f} ms  {fl/ms/1e9:8.1f} TFLOP/s  sm {bench.mhz:6.0f} MHz  per-clock {100*eff:5.1f}%")
