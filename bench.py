@@ -41,8 +41,11 @@ CONFIGS = {
     "multilayer": dict(E=8, K=2, H=4096, F=14336, T=16384, layers=4, drift=(0.3, 0.15),
                        workload="multi-layer dynamic skew: 4 stacked Mixtral-shape layers with drifting "
                                 "per-iteration routing, planner re-layout every step"),
-    "tiny": dict(E=8, K=2, H=256, F=512, T=512,
-                 workload="tiny FSEP MoE layer: 8 experts top-2, hidden 256, ffn 512, 512 tokens/device"),
+    # configs[0]: 4096 tokens over 8 simulated devices -> on one GPU as 8 emulated ranks running the
+    # shipped multi-GPU transport (MP_FSEP_FLAG_COPY_ENGINE), C=2, planner re-layout every step
+    "tiny": dict(E=8, K=2, H=256, F=512, T=512, virtual_ranks=8, capacity=2,
+                 workload="tiny FSEP MoE layer: 8 experts top-2, hidden 256, ffn 512, 4096 tokens over 8 simulated "
+                          "devices (8 emulated ranks on one GPU), Zipf(1.2)"),
 }
 SEED_DATA, SEED_PLANNER = 42, 7
 
@@ -119,71 +122,105 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU paths
-def cpu_reference_rate(cfg, N, C, alpha, sample_tokens, steps=1):
-    """Reference CPU path on a bounded sample: reference planner (oracle/_ref, 1 core)
-    + numpy fp32 layer restatement (all cores).  Returns (tokens/s, details)."""
-    from oracle import layer_oracle as LO
-    from oracle import ref as REF
-    E, K, H, F = cfg["E"], cfg["K"], cfg["H"], cfg["F"]
-    rng = np.random.default_rng(SEED_DATA)
-    bf = LO.bf16_round
-    nrm = lambda *shape: rng.standard_normal(size=shape, dtype=np.float32)
-    wg = bf(nrm(E, H) * 0.02)
-    w1 = np.stack([bf(nrm(F, H) / np.float32(np.sqrt(H))) for _ in range(E)])
-    w3 = np.stack([bf(nrm(F, H) / np.float32(np.sqrt(H))) for _ in range(E)])
-    w2 = np.stack([bf(nrm(H, F) / np.float32(np.sqrt(F))) for _ in range(E)])
-    perm = rng.permutation(E)
-    x = bf(nrm(sample_tokens, H))
-    dy = bf(nrm(sample_tokens, H) * 0.1)
-    bias = zipf_bias(rng, sample_tokens, E, alpha, perm)
-    # planner on the full-size histogram of this workload (the reference's per-layer-step call)
-    R = np.stack([np.bincount(LO.topk(zipf_bias(rng, 4096, E, alpha, perm), K)[0].reshape(-1), minlength=E)
-                  for _ in range(N)]) * (cfg["T"] // 4096 if cfg["T"] >= 4096 else 1)
-    plan_s = 0.0
-    have_ref = REF.available()
-    if have_ref and N > 1:
-        res = REF.plan_bench(R.tolist(), C, 50, bandwidth=9e11, v_comm=2.0 * H, v_comp=6.0 * H * F, b_comp=1.6354e15)
-        plan_s = (res["plan_us"] + res["route_us"]) * 1e-6
-    times = []
-    for _ in range(steps):
+class CpuReference:
+    """The reference CPU path of one layer step, timed on the host cores.
+
+    The reference ships no GPU executor: its CPU path for a layer step
+    is the reference planner itself (oracle/_ref = the unmodified reference library:
+    plan_layout + lite_routing on the step's histogram, 1 core, timed by the
+    reference-linked oracle/refplan_bench) plus the CPU restatement of the layer
+    math (oracle/layer_oracle.py, numpy fp32, BLAS on all cores).  A step processes
+    `sample` tokens in full (all tokens of the workload for the tiny config, a
+    bounded sample of the same workload otherwise) and is measured, not modelled:
+    tokens/s = sample / (layer-math seconds + planner seconds)."""
+
+    def __init__(self, cfg, N, C, alpha, sample):
+        from oracle import layer_oracle as LO
+        from oracle import ref as REF
+        self.LO, self.REF = LO, REF
+        E, K, H, F = cfg["E"], cfg["K"], cfg["H"], cfg["F"]
+        self.N, self.C, self.K, self.H, self.F, self.E = N, C, K, H, F, E
+        rng = np.random.default_rng(SEED_DATA)
+        bf = LO.bf16_round
+        nrm = lambda *shape: rng.standard_normal(size=shape, dtype=np.float32)
+        self.wg = bf(nrm(E, H) * 0.02)
+        self.w1 = np.stack([bf(nrm(F, H) / np.float32(np.sqrt(H))) for _ in range(E)])
+        self.w3 = np.stack([bf(nrm(F, H) / np.float32(np.sqrt(H))) for _ in range(E)])
+        self.w2 = np.stack([bf(nrm(H, F) / np.float32(np.sqrt(F))) for _ in range(E)])
+        perm = rng.permutation(E)
+        ranks = N if sample >= N * cfg["T"] else 1  # full tiny step: every simulated rank's tokens
+        per = sample // ranks
+        self.xs = [bf(nrm(per, H)) for _ in range(ranks)]
+        self.dys = [bf(nrm(per, H) * 0.1) for _ in range(ranks)]
+        self.bias = [zipf_bias(rng, per, E, alpha, perm) for _ in range(ranks)]
+        self.sample = per * ranks
+        self.full = ranks == N and N > 1
+        # the planner's input: the histogram of the full-size step (every rank's T tokens)
+        scale = cfg["T"] // 4096 if cfg["T"] >= 4096 else 1
+        tk = min(cfg["T"], 4096)
+        self.R = np.stack([np.bincount(LO.topk(zipf_bias(rng, tk, E, alpha, perm), K)[0].reshape(-1), minlength=E)
+                           for _ in range(N)]) * scale
+        self.planner = N > 1 and REF.available()
+        self.A = None
+        if self.full:
+            from paper_2602_11686_b200 import planner as PL
+            self.A = PL.even_replication_layout(N, E, C)
+
+    def step(self):
+        """One measured step; returns (seconds, tokens, planner seconds)."""
+        plan_s = 0.0
+        if self.planner:
+            res = self.REF.plan_bench(self.R.tolist(), self.C, 20, bandwidth=9e11, v_comm=2.0 * self.H,
+                                      v_comp=6.0 * self.H * self.F, b_comp=1.6354e15)
+            plan_s = (res["plan_us"] + res["route_us"]) * 1e-6
         t0 = time.perf_counter()
-        LO.layer_step([x], [bias], wg, w1, w3, w2, K, None, C, [dy], dtype=np.float32)
-        times.append(time.perf_counter() - t0)
-    layer_s = min(times)
-    # one layer step covers N*T tokens at the planner's cost once per step
-    per_token = layer_s / sample_tokens
-    step_s = (per_token * N * cfg["T"] + plan_s) * cfg.get("layers", 1)
-    rate = N * cfg["T"] / step_s
-    detail = {"layer_s_per_token": per_token, "planner_us_per_step": plan_s * 1e6, "planner": "oracle/_ref"
-              if have_ref and N > 1 else "not needed at N=1 (C=E, single layout)"}
-    return rate, detail, layer_s
+        self.LO.layer_step(self.xs, self.bias, self.wg, self.w1, self.w3, self.w2, self.K, self.A, self.C, self.dys,
+                           dtype=np.float32)
+        layer_s = time.perf_counter() - t0
+        return layer_s + plan_s, self.sample, plan_s
+
+    def describe(self, cfg_name):
+        planner = ("reference plan_layout + lite_routing (oracle/_ref, 1 core) on the step's N x E histogram"
+                   if self.planner else "no planner call (N=1: one device hosts every expert)")
+        what = (f"all {self.sample} tokens of the {cfg_name} step ({self.N} simulated ranks, routed through "
+                f"lite_routing into the planned layout)" if self.full else
+                f"{self.sample} tokens of the {cfg_name} workload per step")
+        return (f"{what}: layer math via oracle/layer_oracle.py (numpy fp32, BLAS on {os.cpu_count()} cores) + "
+                f"{planner}; measured per step, tokens/s = tokens / step seconds")
+
+
+def cpu_sample_tokens(cfg, N, budget_flops):
+    if cfg.get("virtual_ranks"):
+        return cfg["virtual_ranks"] * cfg["T"]  # the tiny step in full
+    return max(64, min(2048, int(budget_flops / (18 * cfg["K"] * cfg["H"] * cfg["F"]))))
 
 
 def run_reference_impl(args, cfg):
-    N = args.gpus
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    C = args.capacity or default_capacity(cfg["E"], cfg["K"], N)
-    sample = args.cpu_sample or max(64, min(1024, int(4.0e12 / (18 * cfg["K"] * cfg["H"] * cfg["F"]))))
-    ncores = os.cpu_count()
-    ts = []
-    rate = None
+    N = cfg.get("virtual_ranks") or args.gpus
+    C = args.capacity or cfg.get("capacity") or default_capacity(cfg["E"], cfg["K"], N)
+    sample = args.cpu_sample or cpu_sample_tokens(cfg, N, 2.0e12)
+    ref = CpuReference(cfg, N, C, args.alpha, sample)
+    ts, toks, plan = [], 0, 0.0
     for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        rate, detail, _ = cpu_reference_rate(cfg, N, C, args.alpha, sample)
+        sec, n, ps = ref.step()
         if i >= args.warmup:
-            ts.append(time.perf_counter() - t0)
-    cpu = {"value": rate, "unit": "tokens/s", "cores": ncores, "kind": "port",
-           "sample": f"{sample} tokens/step of the {args.config} workload through oracle/layer_oracle.py "
-                     f"(numpy fp32, BLAS on {ncores} cores) + reference plan_layout+lite_routing "
-                     f"(oracle/_ref, 1 core) per layer-step; tokens/s extrapolated to {N}x{cfg['T']} tokens"}
-    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "tokens/s", "n_gpus": N,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": N * cfg["T"] / rate * 1e3,
+            ts.append(sec)
+            toks += n
+            plan += ps
+    rate = toks / sum(ts)
+    ncores = os.cpu_count()
+    cpu = {"value": rate, "unit": "tokens/s", "cores": ncores, "kind": "port", "sample": ref.describe(args.config),
+           "planner_us_per_step": round(plan / len(ts) * 1e6, 2)}
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum(ts) / len(ts) * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Gumbel-top-k Zipf routing, random-init weights)",
             "config": {"workload": cfg["workload"], "n_experts": cfg["E"], "top_k": cfg["K"], "hidden": cfg["H"],
-                       "ffn": cfg["F"], "tokens_per_gpu": cfg["T"], "capacity": C, "zipf_alpha": args.alpha},
+                       "ffn": cfg["F"], "tokens_per_gpu": cfg["T"], "capacity": C, "zipf_alpha": args.alpha,
+                       "tokens_per_step_measured": ref.sample},
             "cpu_baseline": cpu,
             "e2e": {"value": rate, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -259,6 +296,9 @@ def main():
     ap.add_argument("--no-prefetch", action="store_true",
                     help="multi-layer: do not chain layers (each layer restores at its own forward)")
     ap.add_argument("--no-phases", action="store_true", help="skip per-phase device timing events")
+    ap.add_argument("--defer-rs", action="store_true",
+                    help="multi-layer: complete each layer's gradient reduce-scatter under the previous layer's "
+                         "backward (PAPER Fig.5(e))")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.tokens:
@@ -279,10 +319,13 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    N = world
+    # V > 0: the configuration's N ranks are emulated on this one GPU (tiny config)
+    V = cfg.get("virtual_ranks", 0) if world == 1 else 0
+    N = V or world
     E, K, H, F, T = cfg["E"], cfg["K"], cfg["H"], cfg["F"], cfg["T"]
-    C = args.capacity or default_capacity(E, K, N)
+    C = args.capacity or cfg.get("capacity") or default_capacity(E, K, N)
     L = cfg.get("layers", 1)
+    RT = (V or 1) * T  # token rows this process feeds per step
 
     from paper_2602_11686_b200 import planner as PL
     from paper_2602_11686_b200.layer import FsepLayer, LayerSpec
@@ -293,9 +336,9 @@ def main():
     def make_layers(cap, layout, resident=False, local_first=False):
         out = []
         for l in range(L):
-            layer = FsepLayer(LayerSpec(E, K, H, F, T, cap, world=N, rank=rank, virtual=False, resident=resident,
-                                        local_first=local_first))
-            if N > 1:
+            layer = FsepLayer(LayerSpec(E, K, H, F, T, cap, world=N, rank=rank, virtual=V > 0, resident=resident,
+                                        local_first=local_first, copy_engine=V > 0, defer_rs=args.defer_rs))
+            if world > 1:
                 layer.connect_torch_distributed()
             # random-init weights of the named architecture (identical on every rank)
             g = torch.Generator(device="cuda").manual_seed(SEED_DATA + 7919 * l)
@@ -321,8 +364,8 @@ def main():
     # Gumbel-top-k with Zipf(alpha) popularity, or (multi-layer config) the drifting per-iteration
     # popularity of the reference trace generator (generate_trace: Dirichlet(0.3) init, sigma 0.15 walk).
     gx = torch.Generator(device="cuda").manual_seed(SEED_DATA * 1000 + rank)
-    x = torch.randn(T, H, device="cuda", generator=gx).bfloat16()
-    dy = (torch.randn(T, H, device="cuda", generator=gx) * 0.1).bfloat16()
+    x = torch.randn(RT, H, device="cuda", generator=gx).bfloat16()
+    dy = (torch.randn(RT, H, device="cuda", generator=gx) * 0.1).bfloat16()
     rng = np.random.default_rng(SEED_DATA + rank)
     n_bias = args.warmup + args.steps if cfg.get("drift") else 4
     if cfg.get("drift"):
@@ -330,27 +373,38 @@ def main():
                            "tokens_per_device": T, "skew_alpha": cfg["drift"][0], "drift_sigma": cfg["drift"][1],
                            "seed": SEED_DATA})
         logp = np.log(np.maximum(PL.trace_popularity(spec), 1e-30))
-        gum = [rng.gumbel(size=(T, E)) for _ in range(4)]
+        gum = [rng.gumbel(size=(RT, E)) for _ in range(4)]
         bias_h = [[torch.from_numpy((logp[l, i][None, :] + gum[(i + l) % 4]).astype(np.float32)).pin_memory()
                    for i in range(n_bias)] for l in range(L)]
     else:
         perm = np.random.default_rng(SEED_DATA).permutation(E)  # same popularity order on all ranks
-        bias_h = [[torch.from_numpy(zipf_bias(rng, T, E, args.alpha, perm)).pin_memory() for _ in range(n_bias)]
+        bias_h = [[torch.from_numpy(zipf_bias(rng, RT, E, args.alpha, perm)).pin_memory() for _ in range(n_bias)]
                   for _ in range(L)]
     bias_d = [[b.cuda() for b in row] for row in bias_h]
     ys = [torch.empty_like(x) for _ in range(L)]
     dxs = [torch.empty_like(x) for _ in range(L)]
     stream = torch.cuda.current_stream()
 
-    def run_step(i, xin, dyin, biases):
+    def run_step(i, xin, dyin, biases, y_last=None, dx_first=None):
         h = xin
         for l, layer in enumerate(layers):
-            layer.forward(h, biases[l][i % n_bias], T, ys[l])
-            h = ys[l]
+            out = y_last if (l == L - 1 and y_last is not None) else ys[l]
+            layer.forward(h, biases[l][i % n_bias], T, out)
+            h = out
         gr = dyin
         for l in reversed(range(L)):
-            layers[l].backward(gr, dxs[l])
-            gr = dxs[l]
+            out = dx_first if (l == 0 and dx_first is not None) else dxs[l]
+            layers[l].backward(gr, out)
+            gr = out
+
+    def assert_healthy(tag):
+        # a step with a device-detected failure (receive overflow, barrier or readiness
+        # timeout) must not produce a bench line: MP_ERR_DEVICE raises here, on every rank
+        for l, layer in enumerate(layers):
+            try:
+                layer.check()
+            except Exception as exc:
+                raise SystemExit(f"bench: {tag}: layer {l} on rank {rank} failed on the device: {exc}")
 
     def step(i):
         run_step(i, x, dy, bias_d)
@@ -383,6 +437,7 @@ def main():
             layer.stats_reset()
         ms = timed(args.steps, lambda i: step(args.warmup + i))
     clocks = clk.result
+    assert_healthy("timed steps")
     sts = [layer.stats() for layer in layers]
     phases = layers[0].phase_ms() if os.environ.get("FSEP_PHASE_TIMING") == "1" else None
     if phases:
@@ -401,12 +456,13 @@ def main():
         per_rank["recv_rows_last_step"] = [a["rows"] for a in allp]
     st = {"gemm_ms": sum(s_["gemm_ms"] for s_ in sts), "gemm_flops": sum(s_["gemm_flops"] for s_ in sts),
           "kernel_launches": sum(s_["kernel_launches"] for s_ in sts)}
-    value = N * T / (ms * 1e-3)
+    value = N * T / (ms * 1e-3)  # whole job: every rank's (or emulated rank's) T tokens
 
     # ---- roofline of the dominant kernel class (grouped tcgen05 GEMMs)
     burst, sustained, hbm, src = peaks()
     gemm_tflops = st["gemm_flops"] / (st["gemm_ms"] * 1e-3) / 1e12
     flop_tok = 18.0 * K * H * F * L
+    n_dev = world  # physical GPUs the step ran on
     traffic = None
     prof = ROOT / "profiles" / f"gemm_traffic_{args.config}.json"
     if prof.exists():
@@ -421,7 +477,7 @@ def main():
                 "flops_per_step": st["gemm_flops"], "gemm_ms_per_step": round(st["gemm_ms"], 4),
                 "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained ({src}); burst {burst}",
                 "frac_of_burst": round(gemm_tflops / burst, 4),
-                "step_frac": round(value / N * flop_tok / (sustained * 1e12), 4)}
+                "step_frac": round(value / n_dev * flop_tok / (sustained * 1e12), 4)}
 
     # ---- end-to-end through the public API with host buffers
     e2e = None
@@ -431,13 +487,20 @@ def main():
         # i+1's upload overlaps step i's compute) and a result metric is read back.
         x_h = x.cpu().pin_memory()
         dy_h = dy.cpu().pin_memory()
-        metric_h = torch.empty(2, dtype=torch.float32).pin_memory()
         bufs = [(torch.empty_like(x), torch.empty_like(dy), [torch.empty_like(bias_d[0][0]) for _ in range(L)])
                 for _ in range(2)]
+        # the step's outputs (last layer's y, first layer's dx) come back to pinned host memory
+        # every step on a D2H stream, double-buffered so step i's copy overlaps step i+1
+        outs = [(torch.empty_like(x), torch.empty_like(x)) for _ in range(2)]
+        outs_h = [(torch.empty(x.shape, dtype=x.dtype).pin_memory(), torch.empty(x.shape, dtype=x.dtype).pin_memory())
+                  for _ in range(2)]
         copy_stream = torch.cuda.Stream()
+        d2h_stream = torch.cuda.Stream()
         ready = [torch.cuda.Event() for _ in range(2)]
         free = [torch.cuda.Event() for _ in range(2)]
-        for ev in free:
+        computed = [torch.cuda.Event() for _ in range(2)]
+        drained = [torch.cuda.Event() for _ in range(2)]
+        for ev in free + drained:
             ev.record(stream)
 
         def upload(i):
@@ -459,21 +522,29 @@ def main():
             # this step's copy-engine restore / reduce-scatter pushes
             upload(i + 1)
             stream.wait_event(ready[b])
+            stream.wait_event(drained[b])  # step i-2's outputs have left this buffer
             xb, dyb, bb = bufs[b]
-            run_step(0, xb, dyb, [[t] for t in bb])
+            run_step(0, xb, dyb, [[t] for t in bb], y_last=outs[b][0], dx_first=outs[b][1])
             free[b].record(stream)
-            m = torch.stack([ys[-1].sum(dtype=torch.float32), dxs[0].sum(dtype=torch.float32)])
-            metric_h.copy_(m, non_blocking=True)
+            computed[b].record(stream)
+            d2h_stream.wait_event(computed[b])
+            with torch.cuda.stream(d2h_stream):
+                outs_h[b][0].copy_(outs[b][0], non_blocking=True)
+                outs_h[b][1].copy_(outs[b][1], non_blocking=True)
+            drained[b].record(d2h_stream)
 
         for i in range(args.warmup):
             e2e_step(i)
         torch.cuda.synchronize()
-        ems = timed(args.steps, e2e_step)
+        ems = timed(args.steps, e2e_step)  # its closing synchronize waits for the last D2H
+        assert_healthy("e2e steps")
         bi = x.numel() * 2 + dy.numel() * 2 + L * bias_d[0][0].numel() * 4
-        e2e = {"value": N * T / (ems * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": 8,
+        bo = 2 * x.numel() * 2
+        e2e = {"value": N * T / (ems * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
                "ms_per_step": ems,
-               "note": "x, dy, routing bias H2D from pinned host memory every step (double-buffered copy stream) "
-                       "+ [sum y, sum dx] D2H per step, inside the timed region"}
+               "note": "x, dy, routing bias H2D from pinned host memory every step (double-buffered copy stream); "
+                       "the step's outputs y (last layer) and dx (first layer) D2H into pinned host memory every "
+                       "step (double-buffered D2H stream); all inside the timed region"}
 
     # ---- static-EP comparison (same kernels, static_ep_layout at the same C)
     static = None
@@ -484,6 +555,7 @@ def main():
         for i in range(args.warmup):
             step(i)
         sms = timed(args.steps, lambda i: step(args.warmup + i))
+        assert_healthy("static-EP steps")
         static = {"value": N * T / (sms * 1e-3), "ms_per_step": sms, "layout": "static_ep_layout(N,E,C)",
                   "speedup_laer_over_static": round(sms / ms, 4)}
 
@@ -498,6 +570,7 @@ def main():
         for i in range(args.warmup):
             step(i)
         ems_ = timed(args.steps, lambda i: step(args.warmup + i))
+        assert_healthy("pure-EP steps")
         pure_ep = {"value": N * T / (ems_ * 1e-3), "ms_per_step": ems_, "capacity": E // N,
                    "layout": "static_ep_layout(N,E,E/N), experts resident, no restore / reduce-scatter",
                    "speedup_laer_over_ep": round(ems_ / ms, 4)}
@@ -512,21 +585,22 @@ def main():
         for i in range(args.warmup):
             step(i)
         lms = timed(args.steps, lambda i: step(args.warmup + i))
+        assert_healthy("local-first steps")
         local_first = {"value": N * T / (lms * 1e-3), "ms_per_step": lms,
                        "routing": "local-first (non-parity variant): sources hosting a replica keep their tokens",
                        "speedup_over_lite_routing": round(ms / lms, 4)}
 
     # ---- CPU baseline (rank 0 at N=1 only)
     cpu = None
-    if rank == 0 and N == 1 and not args.no_cpu:
-        sample = args.cpu_sample or max(64, min(2048, int(8.0e12 / (18 * K * H * F))))
-        rate, detail, secs = cpu_reference_rate(cfg, N, C, args.alpha, sample)
-        cpu = {"value": rate, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": f"{sample} tokens of the workload through oracle/layer_oracle.py (numpy fp32 BLAS, "
-                         f"{os.cpu_count()} cores, {secs:.1f}s); planner: {detail['planner']}; extrapolated"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        ref = CpuReference(cfg, N, C, args.alpha, args.cpu_sample or cpu_sample_tokens(cfg, N, 2.0e12))
+        sec, ntok, ps = ref.step()
+        cpu = {"value": ntok / sec, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": ref.describe(args.config), "seconds": round(sec, 3),
+               "planner_us_per_step": round(ps * 1e6, 2)}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": N, "steps": args.steps,
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic: x~N(0,1) bf16, random-init weights, Gumbel-top-k routing with Zipf popularity",
@@ -535,9 +609,11 @@ def main():
                            "routing": ("drifting trace popularity alpha=%g sigma=%g" % tuple(cfg["drift"]))
                            if cfg.get("drift") else f"Zipf({args.alpha}) Gumbel-top-k",
                            "layout": args.layout if N > 1 else "single device (C=E)",
+                           "emulated_ranks": V or None,
                            "token_routing": "lite_routing (reference, planner.cpp:238-287)" if args.routing == "lite"
                            else "local-first (non-parity variant)",
-                           "parallelism": f"fsep{N}",
+                           "parallelism": f"fsep{N}" + (" (emulated on 1 GPU)" if V else ""),
+                           "defer_rs": bool(args.defer_rs),
                            "cross_layer_prefetch": L > 1 and N > 1 and not args.no_prefetch, "l2": "inputs larger than L2 (x 128 MiB + weights)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": st["kernel_launches"] *
                 args.steps, "clocks": clocks}

@@ -5,6 +5,8 @@ import numpy as np
 import pytest
 import torch
 
+from paper_2602_11686_b200._lib import MoeplanError
+
 from oracle import layer_oracle as LO
 from paper_2602_11686_b200 import planner as PL
 from paper_2602_11686_b200.layer import FsepLayer, LayerSpec
@@ -114,9 +116,11 @@ def test_receive_overflow_is_flagged_and_memory_safe():
     x, dy, bias = _inputs(N, T, H, E, 1.5, seed=3)
     y, dx = torch.empty_like(x), torch.empty_like(x)
     small.forward(x, bias, T, y)
-    small.backward(dy, dx)
     torch.cuda.synchronize()
     assert any(small.read("status", v).view(np.int32)[0] == 1 for v in range(N))
+    with pytest.raises(MoeplanError) as ei:  # loud: the failed step is reported (MP_ERR_DEVICE)
+        small.backward(dy, dx)
+    assert ei.value.status == 7
     small.close()
     ok = _layer(N, E, K, H, F, T, C)
     ok.set_layout(PL.even_replication_layout(N, E, C))
