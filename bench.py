@@ -548,7 +548,7 @@ def main():
 
     # ---- static-EP comparison (same kernels, static_ep_layout at the same C)
     static = None
-    if N > 1 and args.layout == "laer" and not args.no_static:
+    if N > 1 and not V and args.layout == "laer" and not args.no_static:
         for layer in layers:
             layer.detach_planner()
             layer.set_layout(PL.static_ep_layout(N, E, C))
@@ -562,7 +562,7 @@ def main():
     # ---- pure expert parallelism: C = E/N, one host per expert, experts
     # resident across steps, no restore and no gradient reduce-scatter -- same kernels
     pure_ep = None
-    if N > 1 and args.layout == "laer" and not args.no_ep and E % N == 0:
+    if N > 1 and not V and args.layout == "laer" and not args.no_ep and E % N == 0:
         for layer in layers:
             layer.close()
         torch.cuda.empty_cache()
@@ -577,7 +577,7 @@ def main():
 
     # ---- local-first token routing (NOT the reference lite_routing)
     local_first = None
-    if N > 1 and args.layout == "laer" and args.routing == "lite" and not args.no_local_first:
+    if N > 1 and not V and args.layout == "laer" and args.routing == "lite" and not args.no_local_first:
         for layer in layers:
             layer.close()
         torch.cuda.empty_cache()

@@ -243,6 +243,10 @@ mp_status mp_fsep_layer_check(mp_fsep_layer* layer, uint32_t* bits);
  * the next restore skips one readiness flag -> bit 2), "barrier_timeout"
  * (virtual mode: emulated rank 0 enters a peer barrier alone -> bit 1). */
 mp_status mp_fsep_layer_debug_inject(mp_fsep_layer* layer, const char* what);
+/* Transport probe: `iters` back-to-back full shard restores of the current layout
+ * through the push transport (copy engines, or the SM push kernel with
+ * FSEP_COMM=sm), each closed by a cross-rank barrier; *ms = mean time per restore. */
+mp_status mp_fsep_layer_debug_restore(mp_fsep_layer* layer, int iters, double* ms);
 
 /* Capture forward+backward into a CUDA graph and replay it (bench path). */
 mp_status mp_fsep_layer_graph_step(mp_fsep_layer* layer, const void* x, const float* bias, uint32_t n_tokens,

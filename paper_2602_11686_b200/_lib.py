@@ -100,6 +100,7 @@ _SIGS = {
     "mp_fsep_layer_graph_step": (C.c_int, [vp, vp, vp, u32, vp, vp, vp, vp]),
     "mp_fsep_layer_check": (C.c_int, [vp, C.POINTER(u32)]),
     "mp_fsep_layer_debug_inject": (C.c_int, [vp, cp]),
+    "mp_fsep_layer_debug_restore": (C.c_int, [vp, C.c_int, dblp]),
 }
 
 

@@ -77,7 +77,57 @@ __global__ void peer_barrier_kernel(unsigned int* const* __restrict__ peer_flags
   __syncthreads();
 }
 
+__global__ void __launch_bounds__(256) push_copies_kernel(const CopyTask* __restrict__ tasks, int ntasks,
+                                                         unsigned total_pieces, unsigned long long piece_bytes,
+                                                         unsigned* __restrict__ done) {
+  __shared__ int s_task;
+  for (unsigned p = blockIdx.x; p < total_pieces; p += gridDim.x) {
+    if (threadIdx.x == 0) {
+      int t = 0;
+      while (t + 1 < ntasks && tasks[t + 1].first_piece <= p) ++t;
+      s_task = t;
+    }
+    __syncthreads();
+    const CopyTask& tk = tasks[s_task];
+    const unsigned long long off = static_cast<unsigned long long>(p - tk.first_piece) * piece_bytes;
+    const unsigned long long len = min(piece_bytes, tk.bytes - off);
+    const uint4* __restrict__ src = reinterpret_cast<const uint4*>(static_cast<const char*>(tk.src) + off);
+    uint4* __restrict__ dst = reinterpret_cast<uint4*>(static_cast<char*>(tk.dst) + off);
+    const long long n = static_cast<long long>(len / 16);
+    // 4 independent 16-B loads (local HBM) in flight per thread, then 4 posted stores
+    // (NVLink for a peer destination)
+    constexpr int U = 4;
+    long long i = threadIdx.x;
+    for (; i + (U - 1) * 256 < n; i += U * 256) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = __ldg(src + i + u * 256);
+#pragma unroll
+      for (int u = 0; u < U; ++u) dst[i + u * 256] = v[u];
+    }
+    for (; i < n; i += 256) dst[i] = __ldg(src + i);
+    __threadfence_system();  // this thread's stores are visible system-wide ...
+    __syncthreads();         // ... for every thread of the CTA, before the completion count
+    if (threadIdx.x == 0) {
+      const unsigned pieces = static_cast<unsigned>((tk.bytes + piece_bytes - 1) / piece_bytes);
+      unsigned prev;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(done + s_task) : "memory");
+      if (prev + 1 == pieces && tk.flag != nullptr)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(tk.flag), "r"(tk.flag_val) : "memory");
+    }
+    __syncthreads();  // s_task is rewritten for the next piece
+  }
+}
+
 }  // namespace
+
+void launch_push_copies(const CopyTask* tasks, int ntasks, unsigned total_pieces, unsigned long long piece_bytes,
+                        unsigned* done, int ctas, cudaStream_t st) {
+  if (ntasks == 0 || total_pieces == 0) return;
+  cudaMemsetAsync(done, 0, static_cast<size_t>(ntasks) * sizeof(unsigned), st);
+  push_copies_kernel<<<static_cast<unsigned>(ctas), 256, 0, st>>>(tasks, ntasks, total_pieces, piece_bytes, done);
+  count_launch();
+}
 
 void launch_restore(const uint8_t* layout, int E, int N, int rank, int C, long long S, long long flat,
                     const PeerTable& peers, __nv_bfloat16* restored, int blocks_per_chunk, cudaStream_t st) {

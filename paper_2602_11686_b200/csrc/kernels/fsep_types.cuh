@@ -66,6 +66,20 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 
+// One copy of the SM push transport (comm.cu push_copies_kernel): `bytes` from
+// src to dst (a peer's arena over NVLink, or local memory), split into pieces
+// spread over the CTAs; once every piece has landed the CTA that finished last
+// writes *flag = flag_val with a system-scope release (the destination's
+// readiness word).  first_piece: prefix sum of the tasks' piece counts.
+struct CopyTask {
+  const void* src;
+  void* dst;
+  unsigned long long bytes;  // multiple of 16
+  unsigned* flag;            // nullptr: no readiness flag
+  unsigned flag_val;
+  unsigned first_piece;
+};
+
 struct PlanTables {
   // global view (identical on all ranks)
   int n_hosts[kMaxExperts];

@@ -73,6 +73,14 @@ void launch_unpack_grad(const float* chunk, long long lo, long long hi, int H, i
 void launch_restore(const uint8_t* layout, int E, int N, int rank, int C, long long S, long long flat,
                     const PeerTable& peers, __nv_bfloat16* restored, int blocks_per_chunk, cudaStream_t st);
 
+// SM push transport: all pieces of tasks[0, ntasks) (piece_bytes each, the last
+// piece of a task shorter), grid-strided over `ctas` CTAs of 256 threads that use
+// no shared memory and few registers -- they co-reside with the persistent GEMM
+// (which polls the readiness flags), so the copies overlap it without deadlock.
+// done: ntasks zero-initialised completion counters (zeroed here on `st`).
+void launch_push_copies(const CopyTask* tasks, int ntasks, unsigned total_pieces, unsigned long long piece_bytes,
+                        unsigned* done, int ctas, cudaStream_t st);
+
 // Cross-rank barrier for real multi-GPU mode (system-scope flags in peer memory).
 // Bounded: after timeout_ns the kernel raises kErrBarrierTimeout in err (and flags[world]) and returns.
 void launch_peer_barrier(unsigned int* const* peer_flags, int world, int rank, unsigned int epoch, unsigned* err,

@@ -187,6 +187,17 @@ extern "C" struct mp_fsep_layer {
   unsigned* err_host = nullptr;
   unsigned* err_dev = nullptr;
   unsigned long long spin_timeout_ns = 10000000000ull;  // FSEP_SPIN_TIMEOUT_MS (barriers, readiness waits)
+  // SM push transport (FSEP_COMM=sm): the same pushes and readiness flags as the copy
+  // engines, issued by push_copies_kernel on the side stream (CopyTask batches in a ring)
+  bool sm_push = false;
+  int push_ctas = 32;
+  unsigned long long piece_bytes = 1ull << 20;
+  static constexpr int kTaskRing = 16;
+  int task_cap = 0, task_next = 0;
+  CopyTask* task_host = nullptr;  // pinned [kTaskRing][task_cap]
+  CopyTask* task_dev = nullptr;   // [kTaskRing][task_cap]
+  unsigned* done_dev = nullptr;   // [kTaskRing][task_cap]
+  cudaEvent_t ev_task[kTaskRing] = {};
   int drop_flag = -1;  // test hook (mp_fsep_layer_debug_inject "drop_restore_flag"): source rank whose
                        // next slot-0 readiness flag is not written
 };
@@ -472,6 +483,30 @@ void snapshot_layout(Layer& L, cudaStream_t st) {
   for (Rank& r : L.ranks) CK(cudaMemcpyAsync(r.layout_dev, snap, static_cast<size_t>(E) * N, cudaMemcpyHostToDevice, st));
 }
 
+// SM push transport: copy `tasks` with push_copies_kernel on the side stream after
+// `st`'s work so far, and record every ev_ce[d] after it (same joins as the copy engines).
+void sm_push(Layer& L, cudaStream_t st, std::vector<CopyTask>& tasks) {
+  if (tasks.empty()) return;
+  if (static_cast<int>(tasks.size()) > L.task_cap) throw Error(ErrorKind::device, "sm push: task batch too large");
+  unsigned pieces = 0;
+  for (CopyTask& t : tasks) {
+    t.first_piece = pieces;
+    pieces += static_cast<unsigned>((t.bytes + L.piece_bytes - 1) / L.piece_bytes);
+  }
+  const int k = L.task_next++ % Layer::kTaskRing;
+  CK(cudaEventSynchronize(L.ev_task[k]));  // the ring slot's previous upload is done
+  CopyTask* h = L.task_host + static_cast<size_t>(k) * L.task_cap;
+  CopyTask* d = L.task_dev + static_cast<size_t>(k) * L.task_cap;
+  std::memcpy(h, tasks.data(), tasks.size() * sizeof(CopyTask));
+  CK(cudaEventRecord(L.ev_fork, st));
+  CK(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
+  CK(cudaMemcpyAsync(d, h, tasks.size() * sizeof(CopyTask), cudaMemcpyHostToDevice, L.side));
+  CK(cudaEventRecord(L.ev_task[k], L.side));
+  launch_push_copies(d, static_cast<int>(tasks.size()), pieces, L.piece_bytes,
+                     L.done_dev + static_cast<size_t>(k) * L.task_cap, L.push_ctas, L.side);
+  for (int p = 0; p < L.N; ++p) CK(cudaEventRecord(L.ev_ce[p], L.side));
+}
+
 // Push restore: each local rank's chunk of every expert goes straight into the
 // restored slot of each rank that hosts it (own slots first), and a flag written
 // into the destination's memory after each copy releases that (slot, source)
@@ -485,6 +520,33 @@ void push_restore(Layer& L, cudaStream_t st, int c0 = 0, int c1 = kMaxExperts) {
   if (c0 == 0) {
     ++L.restore_epoch;
     mark(L, st, kPhRestoreBegin);
+  }
+  if (L.sm_push) {  // slot-major task order: slot c of every destination before slot c+1
+    std::vector<std::vector<int>> theirs(N);
+    for (int d = 0; d < N; ++d) theirs[d] = hosted_experts(L.cur_layout, E, N, d);
+    std::vector<CopyTask> tasks;
+    for (int c = c0; c < std::min(c1, L.C); ++c)
+      for (Rank& r : L.ranks)
+        for (int q = 0; q < N; ++q) {
+          const int d = (r.rank + q) % N;
+          if (c >= static_cast<int>(theirs[d].size())) continue;
+          CopyTask t{};
+          t.src = r.shard + static_cast<long long>(theirs[d][c]) * L.S;
+          t.dst = L.peer_restored[d] + static_cast<long long>(c) * L.flat + static_cast<long long>(r.rank) * L.S;
+          t.bytes = static_cast<unsigned long long>(L.S) * 2;
+          t.flag = L.peer_ready[d] + c * N + r.rank;
+          t.flag_val = L.restore_epoch;
+          if (c == 0 && L.drop_flag == r.rank && d != r.rank) {  // test hook: this flag never arrives
+            L.drop_flag = -1;
+            t.flag = nullptr;
+          }
+          tasks.push_back(t);
+        }
+    sm_push(L, st, tasks);
+    if (L.phase_on)
+      for (int d = 0; d < N; ++d)
+        cudaEventRecord(L.ev_ce_t[static_cast<size_t>(L.step_no % mp_fsep_layer::kPhaseRing)][d], L.side);
+    return;
   }
   CK(cudaEventRecord(L.ev_fork, st));
   for (int d = 0; d < N; ++d) CK(cudaStreamWaitEvent(L.ce[d], L.ev_fork, 0));
@@ -695,6 +757,28 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   // Push this rank's replica-gradient chunks [lo, hi) of the flat vector to their
   // owners' staging rows (copy engines, one stream per owner), after `ev`.
   auto push_grads = [&](cudaEvent_t ev, long long lo, long long hi) {
+    if (L.sm_push) {
+      std::vector<CopyTask> tasks;
+      for (Rank& r : L.ranks) {
+        const std::vector<int> mine = hosted_experts(L.cur_layout, E, N, r.rank);
+        for (int q = 1; q < N; ++q) {
+          const int o = (r.rank + q) % N;
+          const long long a = std::max(lo, static_cast<long long>(o) * L.S);
+          const long long b = std::min(hi, static_cast<long long>(o + 1) * L.S);
+          if (a >= b) continue;
+          for (int c = 0; c < static_cast<int>(mine.size()); ++c) {
+            CopyTask t{};
+            t.src = r.grad_full + static_cast<long long>(c) * L.flat + a;
+            t.dst = L.peer_rs_stage[o] + (static_cast<long long>(mine[c]) * N + r.rank) * L.S + (a - o * L.S);
+            t.bytes = static_cast<unsigned long long>(b - a) * 4;
+            tasks.push_back(t);
+          }
+        }
+      }
+      (void)ev;  // sm_push orders after st's work (the wgrad GEMM) itself
+      sm_push(L, st, tasks);
+      return;
+    }
     for (int o = 0; o < N; ++o) CK(cudaStreamWaitEvent(L.ce[o], ev, 0));
     for (Rank& r : L.ranks) {
       const std::vector<int> mine = hosted_experts(L.cur_layout, E, N, r.rank);
@@ -896,6 +980,10 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     L->ce_mode = L->N > 1 && want_ce && write_value_fn() != nullptr;
     require(!(L->virt && (d.flags & MP_FSEP_FLAG_COPY_ENGINE)) || L->ce_mode || L->N == 1,
             "copy-engine mode unavailable (cuStreamWriteValue32 entry point missing)");
+    L->sm_push = L->ce_mode && comm && std::string(comm) == "sm";
+    if (const char* v = std::getenv("FSEP_PUSH_CTAS")) L->push_ctas = std::max(1, std::atoi(v));
+    if (const char* v = std::getenv("FSEP_PUSH_PIECE_KB"))
+      L->piece_bytes = static_cast<unsigned long long>(std::max(16, std::atoi(v))) * 1024ull;
     if (const char* v = std::getenv("FSEP_SPIN_TIMEOUT_MS"))
       L->spin_timeout_ns = static_cast<unsigned long long>(std::max(1.0, std::atof(v)) * 1e6);
     CK(cudaHostAlloc(&L->err_host, kErrWords * sizeof(unsigned), cudaHostAllocMapped));
@@ -938,6 +1026,14 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
       CK(cudaEventCreateWithFlags(&L->ev_wg, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&L->ev_w2, cudaEventDisableTiming));
       CK(cudaMallocHost(&L->layout_ring, 4 * static_cast<size_t>(L->E) * L->N));
+      if (L->sm_push) {
+        L->task_cap = local * L->N * L->C;
+        const size_t n = static_cast<size_t>(Layer::kTaskRing) * L->task_cap;
+        CK(cudaMallocHost(&L->task_host, n * sizeof(CopyTask)));
+        CK(cudaMalloc(&L->task_dev, n * sizeof(CopyTask)));
+        CK(cudaMalloc(&L->done_dev, n * sizeof(unsigned)));
+        for (auto& e : L->ev_task) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
     }
     CK(cudaMalloc(&L->d_peer_flags, sizeof(unsigned int*) * kMaxRanks));
     CK(cudaMalloc(&L->d_peer_rs_flags, sizeof(unsigned int*) * kMaxRanks));
@@ -982,6 +1078,12 @@ void mp_fsep_layer_free(mp_fsep_layer* L) {
     cudaEventDestroy(L->ev_wg);
     cudaEventDestroy(L->ev_w2);
     cudaFreeHost(L->layout_ring);
+    if (L->sm_push) {
+      cudaFreeHost(L->task_host);
+      cudaFree(L->task_dev);
+      cudaFree(L->done_dev);
+      for (auto e : L->ev_task) cudaEventDestroy(e);
+    }
   }
   for (cudaEvent_t e : {L->ev_fork, L->ev_restored, L->ev_hist, L->ev_planned, L->ev_rs_done}) cudaEventDestroy(e);
   for (auto& ring : L->ev_g)
@@ -1297,6 +1399,37 @@ mp_status mp_fsep_layer_check(mp_fsep_layer* L, uint32_t* bits) {
     const uint32_t b = take_errors(*L);
     if (bits) *bits = b;
     raise_errors(b);
+  });
+}
+
+// Transport probe (dev/bench): `iters` full shard restores of the current layout
+// (barrier, pushes of every slot, join of this rank's pushes, barrier), timed with
+// events on the layer's capture stream.  *ms = mean per restore.
+mp_status mp_fsep_layer_debug_restore(mp_fsep_layer* L, int iters, double* ms) {
+  return guarded([&] {
+    require(L && ms && iters > 0, "mp_fsep_layer_debug_restore: bad argument");
+    require(L->ce_mode, "mp_fsep_layer_debug_restore: push transport (copy engines / SM push) only");
+    CK(cudaSetDevice(L->device));
+    cudaStream_t st = L->cap_stream;
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    snapshot_layout(*L, st);
+    barrier(*L, st);
+    CK(cudaEventRecord(a, st));
+    for (int i = 0; i < iters; ++i) {
+      push_restore(*L, st);
+      for (int p = 0; p < L->N; ++p) CK(cudaStreamWaitEvent(st, L->ev_ce[p], 0));
+      barrier(*L, st);
+    }
+    CK(cudaEventRecord(b, st));
+    CK(cudaEventSynchronize(b));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, a, b));
+    *ms = static_cast<double>(t) / iters;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    poll_errors(*L);
   });
 }
 

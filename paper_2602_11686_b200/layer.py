@@ -188,6 +188,11 @@ class FsepLayer:
         check(st)
         return bits.value
 
+    def debug_restore_ms(self, iters: int = 10) -> float:
+        ms = C.c_double()
+        check(self.lib.mp_fsep_layer_debug_restore(self._h, iters, C.byref(ms)))
+        return ms.value
+
     def debug_inject(self, what: str) -> None:
         check(self.lib.mp_fsep_layer_debug_inject(self._h, what.encode()))
 

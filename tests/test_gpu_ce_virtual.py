@@ -34,8 +34,18 @@ from torch_ref import _rel, layer_ref
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["copy_engine", "sm_push"])
+def transport(request, monkeypatch):
+    """The push transport under test: copy engines (default) or the SM push kernel
+    (FSEP_COMM=sm: push_copies_kernel on a side stream, same readiness flags)."""
+    if request.param == "sm_push":
+        monkeypatch.setenv("FSEP_COMM", "sm")
+        monkeypatch.setenv("FSEP_PUSH_PIECE_KB", "64")  # several pieces per chunk at these sizes
+    return request.param
+
+
 @pytest.mark.parametrize("layout", ["even", "static", "planned"])
-def test_tiny_config_8_ranks_copy_engine(layout):
+def test_tiny_config_8_ranks_copy_engine(layout, transport):
     """configs[0]: E8 top-2, H256, F512, 4096 tokens over 8 ranks, Zipf(1.2), copy-engine transport."""
     N, E, K, H, F, T, C = 8, 8, 2, 256, 512, 512, 2
     pb = make_problem(N, E, K, H, F, T, 1.2, seed=42)
@@ -62,7 +72,7 @@ def test_tiny_config_8_ranks_copy_engine(layout):
     layer.close()
 
 
-def test_fine_grained_topk8_copy_engine():
+def test_fine_grained_topk8_copy_engine(transport):
     """E64 top-8 family (token de-duplication on), 4 ranks, C=16, planned layout."""
     N, E, K, H, F, T, C = 4, 64, 8, 256, 384, 256, 16
     pb = make_problem(N, E, K, H, F, T, 1.2, seed=5)
@@ -75,7 +85,7 @@ def test_fine_grained_topk8_copy_engine():
     layer.close()
 
 
-def test_planner_steps_copy_engine():
+def test_planner_steps_copy_engine(transport):
     """Attached planner, 3 steps, layout changes every step: each restore epoch's
     readiness flags gate the GEMMs of that step only; every step vs the oracle."""
     N, E, K, H, F, T, C = 4, 8, 2, 256, 256, 256, 3
@@ -139,7 +149,7 @@ def _mixtral_n8_run(copy_engine, w, xs, dys, biases, A, E, K, H, F, T, C, N):
     return out
 
 
-def test_mixtral_shape_8_ranks_c2_copy_engine():
+def test_mixtral_shape_8_ranks_c2_copy_engine(transport):
     """Mixtral expert shape (H4096, F14336, E8 top-2), N=8, C=2, 512 tokens per rank:
     copy-engine transport == device-kernel transport bit for bit, and both within 2e-2
     of the torch fp32 reference on the oracle's routing (every output and gradient)."""
@@ -169,6 +179,8 @@ def test_mixtral_shape_8_ranks_c2_copy_engine():
         assert np.array_equal(ce["idx"][v], idx_l[v])
         assert np.array_equal(ce["slot"][v] >> 24, rt.slot_dev[v])
         assert np.array_equal(ce["slot"][v] & 0xFFFFFF, rt.slot_row[v])
+    import os
+    os.environ.pop("FSEP_COMM", None)  # the reference run: device-kernel transport
     kern = _mixtral_n8_run(False, W.get, xs, dys, biases, A, E, K, H, F, T, C, N)
     assert torch.equal(ce["y"], kern["y"]) and torch.equal(ce["dx"], kern["dx"])
     for e in range(E):

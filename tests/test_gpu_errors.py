@@ -71,8 +71,11 @@ def test_overflow_reported_by_next_call():
     layer.close()
 
 
-def test_restore_readiness_timeout_is_reported(monkeypatch):
+@pytest.mark.parametrize("comm", ["ce", "sm"])
+def test_restore_readiness_timeout_is_reported(monkeypatch, comm):
     monkeypatch.setenv("FSEP_SPIN_TIMEOUT_MS", "200")
+    if comm == "sm":
+        monkeypatch.setenv("FSEP_COMM", "sm")
     N, E, K, H, F, T, C = 4, 8, 2, 256, 256, 256, 4
     layer, io = _layer(N, E, K, H, F, T, C, copy_engine=True)
     _step(layer, io)
