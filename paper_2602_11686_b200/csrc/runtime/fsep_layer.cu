@@ -981,6 +981,11 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     require(!(L->virt && (d.flags & MP_FSEP_FLAG_COPY_ENGINE)) || L->ce_mode || L->N == 1,
             "copy-engine mode unavailable (cuStreamWriteValue32 entry point missing)");
     L->sm_push = L->ce_mode && comm && std::string(comm) == "sm";
+    // SM push: one push kernel per restore, launched at the forward's start (while the SMs
+    // are free), so its CTAs are resident before the persistent gate-up GEMM polls the
+    // flags.  A second kernel launched after dispatch could not always get CTAs beside the
+    // GEMM (flags then only landed after the readiness timeout) -- measured, Mixtral N=8.
+    if (L->sm_push && !std::getenv("FSEP_RESTORE_SPLIT")) L->restore_split = false;
     if (const char* v = std::getenv("FSEP_PUSH_CTAS")) L->push_ctas = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("FSEP_PUSH_PIECE_KB"))
       L->piece_bytes = static_cast<unsigned long long>(std::max(16, std::atoi(v))) * 1024ull;
@@ -1348,6 +1353,8 @@ mp_status mp_fsep_layer_read(mp_fsep_layer* L, const char* name, uint32_t vrank,
     else if (n == "restored") src = r.restored, sz = C * static_cast<size_t>(L->flat) * 2;
     else if (n == "grad_full") src = r.grad_full, sz = C * static_cast<size_t>(L->flat) * 4;
     else if (n == "barrier_status") src = r.flags + N, sz = 4;
+    else if (n == "ready" && r.ready) src = r.ready, sz = C * N * 4;  // readiness flags [slot][source]
+    else if (n == "restore_epoch") src = &L->restore_epoch, sz = 4;
     else throw Error(ErrorKind::invalid_argument, "mp_fsep_layer_read: unknown buffer " + n);
     if (needed) *needed = sz;
     if (dst) {

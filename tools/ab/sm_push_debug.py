@@ -22,6 +22,10 @@ for i in range(2):
         layer.check(); ok = "ok"
     except Exception as ex:
         ok = str(ex)[:80]
+        ep = layer.read("restore_epoch").view(np.uint32)[0]
+        print("epoch", ep, "layout", layer.read("layout", 0).reshape(E, N).tolist())
+        for v in range(N):
+            print(" rank", v, "ready[slot][src]", layer.read("ready", v).view(np.uint32).reshape(C, N).tolist())
     layer.backward(dy, dx); torch.cuda.synchronize(); t2 = time.time()
     print(os.environ.get("TAG"), i, f"fwd {1e3*(t1-t0):.1f} ms bwd {1e3*(t2-t1):.1f} ms", ok, flush=True)
 layer.close()
