@@ -167,8 +167,13 @@ extern "C" struct mp_fsep_layer {
   // reduce-scatter gathers run as peer cudaMemcpyAsync on one stream per peer,
   // using no SMs; the forward GEMMs poll per-(slot, peer) readiness flags.
   bool ce_mode = false;
-  cudaStream_t ce[kMaxRanks] = {};
-  cudaEvent_t ev_ce[kMaxRanks] = {};
+  // copy-engine lanes: ce_k streams per destination rank (FSEP_CE_STREAMS), lane d*ce_k + j;
+  // slot / chunk c of destination d travels on lane d*ce_k + c % ce_k
+  static constexpr int kMaxLanes = 4;
+  int ce_k = 1;
+  cudaStream_t ce[kMaxRanks * kMaxLanes] = {};
+  cudaEvent_t ev_ce[kMaxRanks * kMaxLanes] = {};
+  int lanes() const { return N * ce_k; }
   cudaEvent_t ev_wg = nullptr;
   unsigned restore_epoch = 0;
   __nv_bfloat16* peer_restored[kMaxRanks] = {};  // every rank's restored experts (push targets)
@@ -422,7 +427,7 @@ void barrier(Layer& L, cudaStream_t st) {
 // separate rs flags (everyone's pushes landed), then the ascending-device sum.
 void finish_rs_async(Layer& L) {
   if (L.rs_state != 1) return;
-  for (int o = 0; o < L.N; ++o) CK(cudaStreamWaitEvent(L.side, L.ev_ce[o], 0));
+  for (int o = 0; o < L.lanes(); ++o) CK(cudaStreamWaitEvent(L.side, L.ev_ce[o], 0));
   if (!L.virt && L.N > 1)
     launch_peer_barrier(L.d_peer_rs_flags, L.N, L.ranks[0].rank, ++L.rs_epoch, L.err_dev, L.spin_timeout_ns, L.side);
   for (Rank& r : L.ranks)
@@ -504,7 +509,7 @@ void sm_push(Layer& L, cudaStream_t st, std::vector<CopyTask>& tasks) {
   CK(cudaEventRecord(L.ev_task[k], L.side));
   launch_push_copies(d, static_cast<int>(tasks.size()), pieces, L.piece_bytes,
                      L.done_dev + static_cast<size_t>(k) * L.task_cap, L.push_ctas, L.side);
-  for (int p = 0; p < L.N; ++p) CK(cudaEventRecord(L.ev_ce[p], L.side));
+  for (int p = 0; p < L.lanes(); ++p) CK(cudaEventRecord(L.ev_ce[p], L.side));
 }
 
 // Push restore: each local rank's chunk of every expert goes straight into the
@@ -549,7 +554,7 @@ void push_restore(Layer& L, cudaStream_t st, int c0 = 0, int c1 = kMaxExperts) {
     return;
   }
   CK(cudaEventRecord(L.ev_fork, st));
-  for (int d = 0; d < N; ++d) CK(cudaStreamWaitEvent(L.ce[d], L.ev_fork, 0));
+  for (int d = 0; d < L.lanes(); ++d) CK(cudaStreamWaitEvent(L.ce[d], L.ev_fork, 0));
   for (Rank& r : L.ranks) {
     for (int q = 0; q < N; ++q) {
       const int d = (r.rank + q) % N;
@@ -557,20 +562,20 @@ void push_restore(Layer& L, cudaStream_t st, int c0 = 0, int c1 = kMaxExperts) {
       for (int c = c0; c < std::min(c1, static_cast<int>(theirs.size())); ++c) {
         CK(cudaMemcpyAsync(L.peer_restored[d] + static_cast<long long>(c) * L.flat + static_cast<long long>(r.rank) * L.S,
                            r.shard + static_cast<long long>(theirs[c]) * L.S, static_cast<size_t>(L.S) * 2,
-                           cudaMemcpyDeviceToDevice, L.ce[d]));
+                           cudaMemcpyDeviceToDevice, L.ce[d * L.ce_k + c % L.ce_k]));
         if (c == 0 && L.drop_flag == r.rank && d != r.rank) {  // test hook: this flag never arrives
           L.drop_flag = -1;
           continue;
         }
-        if (write_value_fn()(L.ce[d], reinterpret_cast<CUdeviceptr>(L.peer_ready[d] + c * N + r.rank),
+        if (write_value_fn()(L.ce[d * L.ce_k + c % L.ce_k], reinterpret_cast<CUdeviceptr>(L.peer_ready[d] + c * N + r.rank),
                              L.restore_epoch, 0) != CUDA_SUCCESS)
           throw Error(ErrorKind::device, "cuStreamWriteValue32 failed");
       }
     }
   }
   for (int d = 0; d < N; ++d) {
-    CK(cudaEventRecord(L.ev_ce[d], L.ce[d]));
-    if (L.phase_on) cudaEventRecord(L.ev_ce_t[static_cast<size_t>(L.step_no % mp_fsep_layer::kPhaseRing)][d], L.ce[d]);
+    for (int j = 0; j < L.ce_k; ++j) CK(cudaEventRecord(L.ev_ce[d * L.ce_k + j], L.ce[d * L.ce_k + j]));
+    if (L.phase_on) cudaEventRecord(L.ev_ce_t[static_cast<size_t>(L.step_no % mp_fsep_layer::kPhaseRing)][d], L.ce[d * L.ce_k]);
   }
 }
 
@@ -708,7 +713,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
     gemm(L, GemmKind::kFwdDown, r.tm_act_k, r.tm_w2_k, r.tm_w2_k128, g2, st);
   }
   if (restore && ce) {
-    for (int p = 0; p < N; ++p) CK(cudaStreamWaitEvent(st, L.ev_ce[p], 0));  // join (long complete)
+    for (int p = 0; p < L.lanes(); ++p) CK(cudaStreamWaitEvent(st, L.ev_ce[p], 0));  // join (long complete)
     mark(L, st, kPhRestoreEnd);
   }
   CK(cudaEventRecord(L.ev_g[L.step_no % Layer::kRing][1], st));
@@ -779,7 +784,7 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
       sm_push(L, st, tasks);
       return;
     }
-    for (int o = 0; o < N; ++o) CK(cudaStreamWaitEvent(L.ce[o], ev, 0));
+    for (int o = 0; o < L.lanes(); ++o) CK(cudaStreamWaitEvent(L.ce[o], ev, 0));
     for (Rank& r : L.ranks) {
       const std::vector<int> mine = hosted_experts(L.cur_layout, E, N, r.rank);
       for (int q = 1; q < N; ++q) {
@@ -790,10 +795,10 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
         for (int c = 0; c < static_cast<int>(mine.size()); ++c)
           CK(cudaMemcpyAsync(L.peer_rs_stage[o] + (static_cast<long long>(mine[c]) * N + r.rank) * L.S + (a - o * L.S),
                              r.grad_full + static_cast<long long>(c) * L.flat + a, static_cast<size_t>(b - a) * 4,
-                             cudaMemcpyDeviceToDevice, L.ce[o]));
+                             cudaMemcpyDeviceToDevice, L.ce[o * L.ce_k + c % L.ce_k]));
       }
     }
-    for (int o = 0; o < N; ++o) CK(cudaEventRecord(L.ev_ce[o], L.ce[o]));
+    for (int o = 0; o < L.lanes(); ++o) CK(cudaEventRecord(L.ev_ce[o], L.ce[o]));
   };
   const long long w2_lo = 2LL * F * H;
   // Order: dH (SwiGLU' fused), dW13, dW2, dX.  The W13 part of the replica
@@ -852,7 +857,7 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
     mark(L, st, kPhRsBarrier);
     L.rs_state = 1;
   } else if (ce_rs) {
-    for (int o = 0; o < N; ++o) CK(cudaStreamWaitEvent(st, L.ev_ce[o], 0));  // own pushes landed
+    for (int o = 0; o < L.lanes(); ++o) CK(cudaStreamWaitEvent(st, L.ev_ce[o], 0));  // own pushes landed
     mark(L, st, kPhRsPushWait);
     // ... and everyone else's: this barrier also orders every rank's dX GEMM (whose
     // epilogue stored dX rows into our tok_rows) before the unpermute below
@@ -986,6 +991,7 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     // flags.  A second kernel launched after dispatch could not always get CTAs beside the
     // GEMM (flags then only landed after the readiness timeout) -- measured, Mixtral N=8.
     if (L->sm_push && !std::getenv("FSEP_RESTORE_SPLIT")) L->restore_split = false;
+    if (const char* v = std::getenv("FSEP_CE_STREAMS")) L->ce_k = std::clamp(std::atoi(v), 1, mp_fsep_layer::kMaxLanes);
     if (const char* v = std::getenv("FSEP_PUSH_CTAS")) L->push_ctas = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("FSEP_PUSH_PIECE_KB"))
       L->piece_bytes = static_cast<unsigned long long>(std::max(16, std::atoi(v))) * 1024ull;
@@ -1025,8 +1031,10 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     if (const char* v = std::getenv("FSEP_RESTORE_BLOCKS")) L->restore_blocks = std::max(1, std::atoi(v));
     if (L->ce_mode) {
       for (int p = 0; p < L->N; ++p) {
-        CK(cudaStreamCreateWithFlags(&L->ce[p], cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&L->ev_ce[p], cudaEventDisableTiming));
+        for (int j = 0; j < L->ce_k; ++j) {
+          CK(cudaStreamCreateWithFlags(&L->ce[p * L->ce_k + j], cudaStreamNonBlocking));
+          CK(cudaEventCreateWithFlags(&L->ev_ce[p * L->ce_k + j], cudaEventDisableTiming));
+        }
       }
       CK(cudaEventCreateWithFlags(&L->ev_wg, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&L->ev_w2, cudaEventDisableTiming));
@@ -1077,8 +1085,10 @@ void mp_fsep_layer_free(mp_fsep_layer* L) {
   cudaFreeHost(L->err_host);
   if (L->ce_mode) {
     for (int p = 0; p < L->N; ++p) {
-      cudaStreamDestroy(L->ce[p]);
-      cudaEventDestroy(L->ev_ce[p]);
+      for (int j = 0; j < L->ce_k; ++j) {
+        cudaStreamDestroy(L->ce[p * L->ce_k + j]);
+        cudaEventDestroy(L->ev_ce[p * L->ce_k + j]);
+      }
     }
     cudaEventDestroy(L->ev_wg);
     cudaEventDestroy(L->ev_w2);
@@ -1426,7 +1436,7 @@ mp_status mp_fsep_layer_debug_restore(mp_fsep_layer* L, int iters, double* ms) {
     CK(cudaEventRecord(a, st));
     for (int i = 0; i < iters; ++i) {
       push_restore(*L, st);
-      for (int p = 0; p < L->N; ++p) CK(cudaStreamWaitEvent(st, L->ev_ce[p], 0));
+      for (int p = 0; p < L->lanes(); ++p) CK(cudaStreamWaitEvent(st, L->ev_ce[p], 0));
       barrier(*L, st);
     }
     CK(cudaEventRecord(b, st));

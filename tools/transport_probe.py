@@ -38,10 +38,10 @@ for name, (E, K, H, F) in shapes.items():
     S = 3 * H * F // N
     rx = C * S * 2 * (N - 1)
     res = {"C": C, "chunk_MB": round(S * 2 / 1e6, 3), "recv_MB_per_gpu": round(rx / 1e6, 1)}
-    variants = [("copy_engine", {})] + [(f"sm_push_{c}cta", {"FSEP_COMM": "sm", "FSEP_PUSH_CTAS": str(c)})
-                                        for c in (8, 16, 32, 64)]
+    variants = [(f"copy_engine_{k}lane", {"FSEP_CE_STREAMS": str(k)}) for k in (1, 2, 4)] + \
+               [(f"sm_push_{c}cta", {"FSEP_COMM": "sm", "FSEP_PUSH_CTAS": str(c)}) for c in (32, 64, 128)]
     for vname, env in variants:
-        for k in ("FSEP_COMM", "FSEP_PUSH_CTAS"):
+        for k in ("FSEP_COMM", "FSEP_PUSH_CTAS", "FSEP_CE_STREAMS"):
             os.environ.pop(k, None)
         os.environ.update(env)
         layer = FsepLayer(LayerSpec(E, K, H, F, 256, C, world=N, rank=rank))
@@ -58,7 +58,7 @@ for name, (E, K, H, F) in shapes.items():
         layer.close()
         torch.cuda.empty_cache()
         dist.barrier()
-    for k in ("FSEP_COMM", "FSEP_PUSH_CTAS"):
+    for k in ("FSEP_COMM", "FSEP_PUSH_CTAS", "FSEP_CE_STREAMS"):
         os.environ.pop(k, None)
     # NCCL: the same bytes per peer as one all-to-all (own chunk included, as the restore does)
     src = torch.empty(N * C * S, device="cuda", dtype=torch.bfloat16)
