@@ -167,7 +167,12 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
     return v ? std::atoi(v) : 0;
   }();
   if (kind == GemmKind::kBwdWgrad && p.raster == 0) p.raster = wgrad_raster;
-  if (wave_sync && a.wave_sync != nullptr && long_k && !(a.policy & 0x800)) {  // policy bit 11: A/B off
+  static const int wave_kinds = [] {  // FSEP_WAVE_SYNC_KINDS: bit k = wave sync allowed for GemmKind k (A/B)
+    const char* v = std::getenv("FSEP_WAVE_SYNC_KINDS");
+    return v ? static_cast<int>(std::strtol(v, nullptr, 0)) : 0x1F;
+  }();
+  if (wave_sync && a.wave_sync != nullptr && long_k && !(a.policy & 0x800) &&
+      ((wave_kinds >> static_cast<int>(kind)) & 1)) {  // policy bit 11: A/B off
     cudaMemsetAsync(a.wave_sync, 0, kWaveSyncMax * sizeof(int), stream);
     p.wave_sync = a.wave_sync;
   }
