@@ -232,7 +232,10 @@ mp_status mp_fsep_layer_phase_ms(mp_fsep_layer* layer, double* out, uint32_t n);
  *   bit 1  peer barrier timeout (a rank did not arrive within FSEP_SPIN_TIMEOUT_MS,
  *          default 10 s),
  *   bit 2  restore readiness timeout (a restored expert chunk's flag never
- *          arrived; the gate-up GEMM stopped waiting).
+ *          arrived; the gate-up GEMM stopped waiting),
+ *   bit 3  memory guard overwritten (checked by mp_fsep_layer_check only: every
+ *          internal buffer is followed by a 256-byte guard pattern, verified on
+ *          the device -- a kernel wrote past the end of a buffer).
  * Every mp_fsep_layer_forward / _backward / _graph_step / _stats call first
  * reports the words that have landed (MP_ERR_DEVICE, message naming the causes,
  * words cleared).  mp_fsep_layer_check synchronises the device first, so it sees
@@ -241,7 +244,8 @@ mp_status mp_fsep_layer_phase_ms(mp_fsep_layer* layer, double* out, uint32_t n);
 mp_status mp_fsep_layer_check(mp_fsep_layer* layer, uint32_t* bits);
 /* Test hook forcing a failure condition: "drop_restore_flag" (copy-engine mode:
  * the next restore skips one readiness flag -> bit 2), "barrier_timeout"
- * (virtual mode: emulated rank 0 enters a peer barrier alone -> bit 1). */
+ * (virtual mode: emulated rank 0 enters a peer barrier alone -> bit 1),
+ * "overwrite_guard" (one byte past the first buffer -> bit 3). */
 mp_status mp_fsep_layer_debug_inject(mp_fsep_layer* layer, const char* what);
 /* Transport probe: `iters` back-to-back full shard restores of the current layout
  * through the push transport (copy engines, or the SM push kernel with

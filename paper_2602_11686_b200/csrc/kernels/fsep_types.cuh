@@ -53,6 +53,7 @@ enum ErrWord : int {
   kErrRecvOverflow = 0,     // a receive segment did not fit max_recv_rows (segments dropped)
   kErrBarrierTimeout = 1,   // a peer barrier timed out (a rank did not arrive)
   kErrRestoreTimeout = 2,   // a restored expert chunk's readiness flag never arrived
+  kErrGuard = 3,            // host-detected: a buffer's memory guard was overwritten (mp_fsep_layer_check)
   kErrWords = 4,
 };
 __device__ __forceinline__ void raise_err(unsigned* err, int word) {

@@ -81,6 +81,11 @@ void launch_restore(const uint8_t* layout, int E, int N, int rank, int C, long l
 void launch_push_copies(const CopyTask* tasks, int ntasks, unsigned total_pieces, unsigned long long piece_bytes,
                         unsigned* done, int ctas, cudaStream_t st);
 
+// Memory guards (256 B each, filled with `pattern`): *first_bad = min(index of an
+// overwritten guard) -- initialise it to INT_MAX.
+void launch_guard_check(const unsigned char* const* guards, int n, unsigned char pattern, int* first_bad,
+                        cudaStream_t st);
+
 // Cross-rank barrier for real multi-GPU mode (system-scope flags in peer memory).
 // Bounded: after timeout_ns the kernel raises kErrBarrierTimeout in err (and flags[world]) and returns.
 void launch_peer_barrier(unsigned int* const* peer_flags, int world, int rank, unsigned int epoch, unsigned* err,

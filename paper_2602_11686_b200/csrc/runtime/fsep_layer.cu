@@ -57,14 +57,28 @@ void cuda_check(cudaError_t e, const char* what) {
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// Memory guards (the memcheck stand-in: compute-sanitizer is closed on the GPU pool):
+// every carved buffer is followed by kGuardBytes of 0xA5; mp_fsep_layer_check verifies
+// them on the device, so a kernel writing past any buffer's end fails the step loudly.
+constexpr size_t kGuardBytes = 256;
+constexpr unsigned char kGuardByte = 0xA5;
+
+struct Guard {
+  const unsigned char* at;
+  const char* after;  // the buffer it follows
+};
+
 struct Carver {
   char* base;
+  std::vector<Guard>* guards;
   size_t off = 0;
   template <typename T>
-  T* take(size_t count) {
+  T* take(size_t count, const char* name) {
     off = align_up(off, 256);
     T* p = reinterpret_cast<T*>(base + off);
     off += count * sizeof(T);
+    guards->push_back({reinterpret_cast<const unsigned char*>(base + off), name});
+    off += kGuardBytes;
     return p;
   }
 };
@@ -103,6 +117,7 @@ struct Rank {
   CUtensorMap tm_w13_k128{}, tm_w2_k128{};  // K-major weight maps with 128-row boxes (CTA-pair kernel)
   CUtensorMap tm_x_k{}, tm_w13_k{}, tm_act_k{}, tm_w2_k{}, tm_dy_k{}, tm_w2_mn{}, tm_dh_k{}, tm_w13_mn{}, tm_dy_mn{},
       tm_act_mn{}, tm_dh_mn{}, tm_x_mn{};
+  std::vector<Guard> guards;  // after every arena / private buffer
   // per-step inputs
   const __nv_bfloat16* x_in = nullptr;
 };
@@ -203,6 +218,9 @@ extern "C" struct mp_fsep_layer {
   CopyTask* task_dev = nullptr;   // [kTaskRing][task_cap]
   unsigned* done_dev = nullptr;   // [kTaskRing][task_cap]
   cudaEvent_t ev_task[kTaskRing] = {};
+  const unsigned char** d_guards = nullptr;  // every local rank's buffer guards (device table)
+  int n_guards = 0;
+  int* d_guard_bad = nullptr;
   int drop_flag = -1;  // test hook (mp_fsep_layer_debug_inject "drop_restore_flag"): source rank whose
                        // next slot-0 readiness flag is not written
 };
@@ -295,101 +313,78 @@ void allocate_rank(Layer& L, Rank& r) {
   const size_t cap = static_cast<size_t>(L.cap);
   const size_t S = static_cast<size_t>(L.S), flat = static_cast<size_t>(L.flat);
   const size_t nblk = (T + kBlockTokens - 1) / kBlockTokens;
-  // arena (peer-visible)
-  size_t a = 0;
-  auto acc = [&](size_t bytes) { a = align_up(a, 256) + bytes; };
-  acc(cap * H * 2);  // x_rows
-  acc(cap * H * 2);  // dy_rows
-  acc(T * K * H * 2);  // tok_rows
-  acc(cap * 4);      // row_src
-  if (L.dedupe) {
-    acc(N * T * H * 2);  // stage
-    acc(cap * 4);        // row_w
-  }
-  acc(N * E * 8);    // R_all
-  acc(C * flat * 4);  // grad_full
-  acc(E * S * 2);    // shard
-  acc((N + 1) * 4);  // flags
-  acc((N + 1) * 4);  // rs_flags
   const bool push = L.ce_mode;
-  if (push) {
-    acc(C * flat * 2);                      // restored (push target)
-    acc(kMaxExperts * kMaxRanks * 4);       // ready
-    acc(E * N * S * 4);                     // rs_stage
-  }
-  r.arena_bytes = align_up(a, 2 << 20);
+  const bool multi = N > 1;
+  const int splits = router_wgrad_splits(static_cast<int>(T));
+  // Each carve runs twice: on a null base to measure the bytes (guards and 256-B
+  // alignment included), then on the allocation.  Identical on every rank, so peer
+  // offsets match.
+  auto carve_arena = [&](Carver& ca) {  // peer-visible
+    r.x_rows = ca.take<__nv_bfloat16>(cap * H, "x_rows");
+    r.dy_rows = ca.take<__nv_bfloat16>(cap * H, "dy_rows");
+    r.tok_rows = ca.take<__nv_bfloat16>(T * K * H, "tok_rows");
+    r.row_src = ca.take<int>(cap, "row_src");
+    if (L.dedupe) {
+      r.stage = ca.take<__nv_bfloat16>(N * T * H, "stage");
+      r.row_w = ca.take<float>(cap, "row_w");
+    }
+    r.R_all = ca.take<unsigned long long>(N * E, "R_all");
+    r.grad_full = ca.take<float>(C * flat, "grad_full");
+    r.shard = ca.take<__nv_bfloat16>(E * S, "shard");
+    r.flags = ca.take<unsigned int>(N + 1, "flags");
+    r.rs_flags = ca.take<unsigned int>(N + 1, "rs_flags");
+    if (push) {
+      r.restored = ca.take<__nv_bfloat16>(C * flat, "restored");  // push target
+      r.ready = ca.take<unsigned>(kMaxExperts * kMaxRanks, "ready");
+      r.rs_stage = ca.take<float>(E * N * S, "rs_stage");
+    }
+  };
+  auto carve_private = [&](Carver& cp) {
+    if (multi) {
+      r.grad_shard = cp.take<float>(E * S, "grad_shard");
+      if (!push) r.restored = cp.take<__nv_bfloat16>(C * flat, "restored");
+    }
+    r.h = cp.take<__nv_bfloat16>(cap * 2 * F, "h");
+    r.act = cp.take<__nv_bfloat16>(cap * F, "act");
+    r.dh = cp.take<__nv_bfloat16>(cap * 2 * F, "dh");
+    r.wg = cp.take<__nv_bfloat16>(E * H, "wg");
+    r.dwg = cp.take<float>(E * H, "dwg");
+    r.dwg_partial = cp.take<float>(static_cast<size_t>(splits) * kDLCols * H, "dwg_partial");  // split-K partials
+    r.dl_dense = cp.take<__nv_bfloat16>((T + 127) / 128 * 128 * kDLCols, "dl_dense");
+    r.rw_rows = cp.take<int>(splits, "rw_rows");
+    r.rw_off = cp.take<int>(splits, "rw_off");
+    r.topk_idx = cp.take<int>(T * K, "topk_idx");
+    r.intra_rank = cp.take<int>(T * K, "intra_rank");
+    r.topk_w = cp.take<float>(T * K, "topk_w");
+    r.dl = cp.take<float>(T * K, "dl");
+    r.slot_dst = cp.take<uint32_t>(T * K, "slot_dst");
+    r.blk_hist = cp.take<int>(nblk * E, "blk_hist");
+    r.blk_base = cp.take<int>(nblk * E, "blk_base");
+    r.layout_dev = cp.take<uint8_t>(E * N, "layout_dev");
+    r.pt = cp.take<PlanTables>(1, "pt");
+    r.wave_sync = cp.take<int>(kWaveSyncMax, "wave_sync");
+  };
+  std::vector<Guard> scratch;
+  Carver measure_a{nullptr, &scratch}, measure_p{nullptr, &scratch};
+  carve_arena(measure_a);
+  carve_private(measure_p);
+  r.arena_bytes = align_up(measure_a.off, 2 << 20);
+  const size_t priv_bytes = align_up(measure_p.off, 2 << 20);
   CK(cudaMalloc(&r.arena, r.arena_bytes));
   CK(cudaMemset(r.arena, 0, r.arena_bytes));
-  Carver ca{static_cast<char*>(r.arena)};
-  r.x_rows = ca.take<__nv_bfloat16>(cap * H);
-  r.dy_rows = ca.take<__nv_bfloat16>(cap * H);
-  r.tok_rows = ca.take<__nv_bfloat16>(T * K * H);
-  r.row_src = ca.take<int>(cap);
-  if (L.dedupe) {
-    r.stage = ca.take<__nv_bfloat16>(N * T * H);
-    r.row_w = ca.take<float>(cap);
-  }
-  r.R_all = ca.take<unsigned long long>(N * E);
-  r.grad_full = ca.take<float>(C * flat);
-  r.shard = ca.take<__nv_bfloat16>(E * S);
-  r.flags = ca.take<unsigned int>(N + 1);
-  r.rs_flags = ca.take<unsigned int>(N + 1);
-  if (push) {
-    r.restored = ca.take<__nv_bfloat16>(C * flat);
-    r.ready = ca.take<unsigned>(kMaxExperts * kMaxRanks);
-    r.rs_stage = ca.take<float>(E * N * S);
-  }
-  // private
-  const int splits = router_wgrad_splits(static_cast<int>(T));
-  size_t b = 0;
-  auto accp = [&](size_t bytes) { b = align_up(b, 256) + bytes; };
-  const bool multi = N > 1;
-  if (multi) {
-    accp(E * S * 4);                    // grad_shard
-    if (!push) accp(C * flat * 2);      // restored
-  }
-  accp(cap * 2 * F * 2);  // h
-  accp(cap * F * 2);      // act
-  accp(cap * 2 * F * 2);  // dh
-  accp(E * H * 2);        // wg
-  accp(E * H * 4);        // dwg
-  accp(static_cast<size_t>(splits) * kDLCols * H * 4);  // dwg_partial (split-K partials)
-  accp((T + 127) / 128 * 128 * kDLCols * 2);  // dl_dense
-  accp(static_cast<size_t>(splits) * 4 * 2);  // rw_rows, rw_off
-  accp(T * K * 4 * 5);    // topk_idx, intra_rank, topk_w, dl, slot_dst
-  accp(nblk * E * 4 * 2);  // blk_hist, blk_base
-  accp(E * N);            // layout
-  accp(sizeof(PlanTables));
-  accp(kWaveSyncMax * sizeof(int));
-  CK(cudaMalloc(&r.priv, align_up(b, 2 << 20)));
-  CK(cudaMemset(r.priv, 0, align_up(b, 2 << 20)));
-  Carver cp{static_cast<char*>(r.priv)};
-  if (multi) {
-    r.grad_shard = cp.take<float>(E * S);
-    if (!push) r.restored = cp.take<__nv_bfloat16>(C * flat);
-  } else {
+  CK(cudaMalloc(&r.priv, priv_bytes));
+  CK(cudaMemset(r.priv, 0, priv_bytes));
+  r.guards.clear();
+  Carver ca{static_cast<char*>(r.arena), &r.guards};
+  carve_arena(ca);
+  Carver cp{static_cast<char*>(r.priv), &r.guards};
+  carve_private(cp);
+  if (!multi) {
     r.grad_shard = r.grad_full;  // one device: the shard IS the full expert set (C == E)
     r.restored = r.shard;
   }
-  r.h = cp.take<__nv_bfloat16>(cap * 2 * F);
-  r.act = cp.take<__nv_bfloat16>(cap * F);
-  r.dh = cp.take<__nv_bfloat16>(cap * 2 * F);
-  r.wg = cp.take<__nv_bfloat16>(E * H);
-  r.dwg = cp.take<float>(E * H);
-  r.dwg_partial = cp.take<float>(static_cast<size_t>(splits) * kDLCols * H);
-  r.dl_dense = cp.take<__nv_bfloat16>((T + 127) / 128 * 128 * kDLCols);
-  r.rw_rows = cp.take<int>(splits);
-  r.rw_off = cp.take<int>(splits);
-  r.topk_idx = cp.take<int>(T * K);
-  r.intra_rank = cp.take<int>(T * K);
-  r.topk_w = cp.take<float>(T * K);
-  r.dl = cp.take<float>(T * K);
-  r.slot_dst = cp.take<uint32_t>(T * K);
-  r.blk_hist = cp.take<int>(nblk * E);
-  r.blk_base = cp.take<int>(nblk * E);
-  r.layout_dev = cp.take<uint8_t>(E * N);
-  r.pt = cp.take<PlanTables>(1);
-  r.wave_sync = cp.take<int>(kWaveSyncMax);
+  // fill the guards (the arenas were zeroed above)
+  for (const Guard& g : r.guards) CK(cudaMemset(const_cast<unsigned char*>(g.at), kGuardByte, kGuardBytes));
   build_maps(L, r);
 }
 
@@ -909,6 +904,7 @@ void raise_errors(uint32_t bits) {
   if (bits & (1u << kErrRecvOverflow)) m += " receive buffer overflow (max_recv_rows too small; segments dropped);";
   if (bits & (1u << kErrBarrierTimeout)) m += " peer barrier timed out (a rank did not arrive);";
   if (bits & (1u << kErrRestoreTimeout)) m += " restored expert chunk never arrived (readiness flag timeout);";
+  if (bits & (1u << kErrGuard)) m += " a kernel wrote past the end of a buffer (memory guard overwritten);";
   throw Error(ErrorKind::device, m);
 }
 
@@ -1007,6 +1003,15 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
       allocate_rank(*L, L->ranks[v]);
     }
     finish_peers(*L);
+    {
+      std::vector<const unsigned char*> all;
+      for (const Rank& r : L->ranks)
+        for (const Guard& g : r.guards) all.push_back(g.at);
+      L->n_guards = static_cast<int>(all.size());
+      CK(cudaMalloc(&L->d_guards, all.size() * sizeof(void*)));
+      CK(cudaMemcpy(L->d_guards, all.data(), all.size() * sizeof(void*), cudaMemcpyHostToDevice));
+      CK(cudaMalloc(&L->d_guard_bad, sizeof(int)));
+    }
     L->connected = L->virt;
     CK(cudaMallocHost(&L->layout_host, static_cast<size_t>(L->E) * L->N));
     CK(cudaMallocHost(&L->R_host, static_cast<size_t>(L->E) * L->N * 8));
@@ -1076,6 +1081,8 @@ void mp_fsep_layer_free(mp_fsep_layer* L) {
   }
   cudaFree(L->d_peer_flags);
   cudaFree(L->d_peer_rs_flags);
+  cudaFree(L->d_guards);
+  cudaFree(L->d_guard_bad);
   cudaFree(L->d_tok_table);
   cudaFreeHost(L->layout_host);
   cudaFreeHost(L->R_host);
@@ -1413,9 +1420,34 @@ mp_status mp_fsep_layer_check(mp_fsep_layer* L, uint32_t* bits) {
     require(L, "mp_fsep_layer_check: NULL layer");
     CK(cudaSetDevice(L->device));
     CK(cudaDeviceSynchronize());
-    const uint32_t b = take_errors(*L);
+    uint32_t b = take_errors(*L);
+    // memory guards after every buffer of every local rank (the memcheck stand-in)
+    std::string guard_msg;
+    if (L->n_guards > 0) {
+      const int none = 0x7fffffff;
+      CK(cudaMemcpy(L->d_guard_bad, &none, sizeof(int), cudaMemcpyHostToDevice));
+      launch_guard_check(L->d_guards, L->n_guards, kGuardByte, L->d_guard_bad, nullptr);
+      int bad = none;
+      CK(cudaMemcpy(&bad, L->d_guard_bad, sizeof(int), cudaMemcpyDeviceToHost));
+      if (bad != none) {
+        b |= 1u << kErrGuard;
+        int idx = bad;
+        for (const Rank& r : L->ranks) {
+          if (idx < static_cast<int>(r.guards.size())) {
+            guard_msg = std::string(" (guard after '") + r.guards[static_cast<size_t>(idx)].after + "' of rank " +
+                        std::to_string(r.rank) + ")";
+            break;
+          }
+          idx -= static_cast<int>(r.guards.size());
+        }
+      }
+    }
     if (bits) *bits = b;
-    raise_errors(b);
+    try {
+      raise_errors(b);
+    } catch (const Error& e) {
+      throw Error(ErrorKind::device, std::string(e.what()) + guard_msg);
+    }
   });
 }
 
@@ -1458,6 +1490,9 @@ mp_status mp_fsep_layer_debug_inject(mp_fsep_layer* L, const char* what) {
     if (w == "drop_restore_flag") {
       require(L->ce_mode, "drop_restore_flag needs copy-engine mode");
       L->drop_flag = L->virt ? 1 : L->ranks[0].rank;  // virtual: emulated rank 1's push to a peer
+    } else if (w == "overwrite_guard") {  // a one-byte overrun past x_rows of the first local rank
+      const Guard& g = L->ranks[0].guards.front();
+      CK(cudaMemset(const_cast<unsigned char*>(g.at), 0, 1));
     } else if (w == "barrier_timeout") {
       require(L->virt && L->N > 1, "barrier_timeout is emulated in virtual mode (rank 0 waits alone)");
       launch_peer_barrier(L->d_peer_flags, L->N, 0, L->epoch + 0x40000000u, L->err_dev, L->spin_timeout_ns, nullptr);

@@ -5,7 +5,8 @@ Forced conditions (one per host-mapped error word, fsep_types.cuh ErrWord):
   * receive-buffer overflow  -- max_recv_rows too small for the routed segments;
   * restore readiness timeout -- a copy-engine readiness flag is never written
     (test hook), the gate-up GEMM's producer gives up after FSEP_SPIN_TIMEOUT_MS;
-  * peer barrier timeout      -- an emulated rank enters a barrier alone.
+  * peer barrier timeout      -- an emulated rank enters a barrier alone;
+  * memory guard overrun      -- a byte past the end of an internal buffer.
 Each is reported by mp_fsep_layer_check and by the next forward; the words are
 cleared once reported, and a clean step afterwards succeeds."""
 import numpy as np
@@ -96,4 +97,21 @@ def test_peer_barrier_timeout_is_reported(monkeypatch):
     _expect_device_error(layer, 1, "peer barrier timed out")
     _step(layer, io)
     assert layer.check() == 0
+    layer.close()
+
+
+def test_memory_guard_overrun_is_reported():
+    """Every internal buffer is followed by a guard pattern checked on the device by
+    mp_fsep_layer_check (the memcheck stand-in on this pool): a one-byte overrun past
+    a buffer fails loudly and names the buffer; clean steps leave every guard intact."""
+    N, E, K, H, F, T, C = 4, 8, 2, 256, 256, 256, 3
+    layer, io = _layer(N, E, K, H, F, T, C, copy_engine=True)
+    for _ in range(2):
+        _step(layer, io)
+    assert layer.check() == 0
+    layer.debug_inject("overwrite_guard")
+    with pytest.raises(MoeplanError) as ei:
+        layer.check()
+    assert ei.value.status == MP_ERR_DEVICE and "x_rows" in str(ei.value)
+    assert layer.last_error_bits == 1 << 3
     layer.close()
