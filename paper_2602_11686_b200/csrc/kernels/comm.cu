@@ -119,14 +119,16 @@ __global__ void __launch_bounds__(256) push_copies_kernel(const CopyTask* __rest
   }
 }
 
-// Memory guards: block g checks the kGuard-byte guard guards[g] (16 x 16 B) against
-// the fill pattern and records the lowest failing guard index.
-__global__ void guard_check_kernel(const unsigned char* const* __restrict__ guards, int n, unsigned pattern4,
+// Memory guards: block g checks the 256-byte guard guards[g] (starts right after a
+// buffer, so any byte alignment: byte loads) against the fill pattern and records the
+// lowest failing guard index.
+__global__ void guard_check_kernel(const unsigned char* const* __restrict__ guards, int n, unsigned char pattern,
                                    int* __restrict__ first_bad) {
   const int g = blockIdx.x;
-  if (g >= n || threadIdx.x >= 16) return;
-  const uint4 v = reinterpret_cast<const uint4*>(guards[g])[threadIdx.x];
-  if (v.x != pattern4 || v.y != pattern4 || v.z != pattern4 || v.w != pattern4) atomicMin(first_bad, g);
+  if (g >= n) return;
+  bool ok = true;
+  for (int i = static_cast<int>(threadIdx.x); i < 256; i += 32) ok &= guards[g][i] == pattern;
+  if (!ok) atomicMin(first_bad, g);
 }
 
 }  // namespace
@@ -134,7 +136,7 @@ __global__ void guard_check_kernel(const unsigned char* const* __restrict__ guar
 void launch_guard_check(const unsigned char* const* guards, int n, unsigned char pattern, int* first_bad,
                         cudaStream_t st) {
   if (n <= 0) return;
-  guard_check_kernel<<<static_cast<unsigned>(n), 32, 0, st>>>(guards, n, 0x01010101u * pattern, first_bad);
+  guard_check_kernel<<<static_cast<unsigned>(n), 32, 0, st>>>(guards, n, pattern, first_bad);
   count_launch();
 }
 
