@@ -8,7 +8,11 @@ one process per GPU, copy-engine communication).  Checks, in real multi-GPU mode
   oracle on the static layout, and a second step (no restore) reproduces the
   first bit for bit;
 * local-first routing (MP_FSEP_FLAG_LOCAL_FIRST): every slot's destination matches
-  the oracle's local-first variant bit for bit.
+  the oracle's local-first variant bit for bit;
+* deferred gradient reduce-scatter (MP_FSEP_FLAG_DEFER_RS, PAPER Fig.5(e)): layer 2's
+  reduce-scatter completed under layer 1's backward gives bit-identical gradients;
+* the SM push transport (FSEP_COMM=sm) is bit-identical to the copy engines;
+* no device-detected failure (barrier / readiness timeouts, overflow, memory guards).
 Exits non-zero on the first mismatch."""
 import json
 import os
@@ -62,9 +66,9 @@ def inputs(rank, step):
     return x, dy, bias
 
 
-def two_layer_steps(world, rank, chain):
+def two_layer_steps(world, rank, chain, defer_rs=False):
     C = 4
-    layers = [make_layer(world, rank, C, weights(11 + l)) for l in range(2)]
+    layers = [make_layer(world, rank, C, weights(11 + l), defer_rs=defer_rs) for l in range(2)]
     for l, layer in enumerate(layers):
         layer.attach_planner(config(world, C), layer=l)
     if chain:
@@ -85,6 +89,7 @@ def two_layer_steps(world, rank, chain):
         grads = [torch.stack(t).cpu() for t in zip(*[layers[1].expert_grad(e) for e in range(E)])]
         outs.append((y2.cpu(), dx1.cpu(), grads))
     for layer in layers:
+        assert layer.check() == 0
         layer.close()
     return outs
 
@@ -98,10 +103,15 @@ def main():
     # 1. chaining is bit-identical to the unchained schedule
     a = two_layer_steps(world, rank, chain=False)
     b = two_layer_steps(world, rank, chain=True)
-    for step, (u, v) in enumerate(zip(a, b)):
-        assert torch.equal(u[0], v[0]) and torch.equal(u[1], v[1]), f"chained outputs differ (step {step})"
-        for gu, gv in zip(u[2], v[2]):
-            assert torch.equal(gu, gv), f"chained gradients differ (step {step})"
+    c = two_layer_steps(world, rank, chain=True, defer_rs=True)
+    os.environ["FSEP_COMM"] = "sm"
+    d = two_layer_steps(world, rank, chain=True)
+    del os.environ["FSEP_COMM"]
+    for tag, other in (("chained", b), ("deferred reduce-scatter", c), ("SM push transport", d)):
+        for step, (u, v) in enumerate(zip(a, other)):
+            assert torch.equal(u[0], v[0]) and torch.equal(u[1], v[1]), f"{tag} outputs differ (step {step})"
+            for gu, gv in zip(u[2], v[2]):
+                assert torch.equal(gu, gv), f"{tag} gradients differ (step {step})"
 
     # 2. pure EP: resident experts, no restore after the first step, no reduce-scatter
     C = E // world
