@@ -106,6 +106,13 @@ void launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p,
 }  // namespace
 
 namespace {
+int env_raster(int kind) {
+  const std::string name = "FSEP_MRASTER_" + std::to_string(kind);
+  const char* v = std::getenv(name.c_str());
+  if (!v) v = std::getenv("FSEP_MRASTER");
+  return v ? std::atoi(v) : 0;
+}
+
 template <bool AMN, bool BMN, bool GK, int EPI>
 void launch_pair(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p, int grid, cudaStream_t st) {
   auto kern = grouped_gemm_pair_kernel<AMN, BMN, GK, EPI>;
@@ -167,6 +174,10 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
     return v ? std::atoi(v) : 0;
   }();
   if (kind == GemmKind::kBwdWgrad && p.raster == 0) p.raster = wgrad_raster;
+  // FSEP_MRASTER[_<kind>]: m-chunk of the M-grouped launches' tile order (A/B; default 16 m tiles,
+  // n-inner: an A chunk of 16 x 256 rows stays in L2 while the B panels stream past it)
+  static const int mraster[4] = {env_raster(0), env_raster(1), env_raster(2), env_raster(3)};
+  if (kind != GemmKind::kBwdWgrad && p.raster == 0) p.raster = mraster[static_cast<int>(kind)];
   static const int wave_kinds = [] {  // FSEP_WAVE_SYNC_KINDS: bit k = wave sync allowed for GemmKind k (A/B)
     const char* v = std::getenv("FSEP_WAVE_SYNC_KINDS");
     return v ? static_cast<int>(std::strtol(v, nullptr, 0)) : 0x1F;
