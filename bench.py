@@ -463,11 +463,12 @@ def main():
     gemm_tflops = st["gemm_flops"] / (st["gemm_ms"] * 1e-3) / 1e12
     flop_tok = 18.0 * K * H * F * L
     n_dev = world  # physical GPUs the step ran on
-    traffic = None
+    traffic = pipe_pct = prof_src = None
     prof = ROOT / "profiles" / f"gemm_traffic_{args.config}.json"
-    if prof.exists():
+    if prof.exists():  # from the committed ncu --set full capture of this config (tools/ncu_summary.py)
         try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+            pj = json.loads(prof.read_text())
+            traffic, pipe_pct, prof_src = pj.get("dram_bytes_per_launch"), pj.get("tensor_pipe_active_pct"), pj.get("source")
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "achieved": round(gemm_tflops, 1), "peak": sustained, "unit": "TFLOP/s",
@@ -477,6 +478,7 @@ def main():
                 "flops_per_step": st["gemm_flops"], "gemm_ms_per_step": round(st["gemm_ms"], 4),
                 "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained ({src}); burst {burst}",
                 "frac_of_burst": round(gemm_tflops / burst, 4),
+                "tensor_pipe_active_pct": pipe_pct, "ncu_source": prof_src,
                 "step_frac": round(value / n_dev * flop_tok / (sustained * 1e12), 4)}
 
     # ---- end-to-end through the public API with host buffers

@@ -54,6 +54,13 @@ mp_status mp_fsep_planner_observe(mp_fsep_planner* planner, const uint64_t* R);
 mp_status mp_fsep_planner_next(mp_fsep_planner* planner, uint8_t* A_out);
 void mp_fsep_planner_free(mp_fsep_planner* planner);
 
+/* SURVEY 8(b)'s mp_fsep_plan_next: the layout for the next step of MoE layer `layer`
+ * from one observed R (history = [R]) with the config's topology / cost / capacity /
+ * planner blocks and the layer-salted seed -- array I/O, no JSON; equals the layout
+ * mp_plan_layer_json reports after an iteration with this R in "last" history mode. */
+mp_status mp_fsep_plan_next(const mp_config* config, const uint64_t* R, uint32_t n_devices, uint32_t layer,
+                            uint8_t* A_out);
+
 /* One-shot plan_layout on a single R (history = [R]) -- the hot call timed in
  * the CPU baseline. seed is used as-is (no layer salting). */
 mp_status mp_fsep_plan_layout(uint32_t n_devices, uint32_t n_experts, uint32_t capacity, double bandwidth,

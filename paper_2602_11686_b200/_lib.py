@@ -66,6 +66,7 @@ _SIGS = {
     "mp_fsep_planner_observe": (C.c_int, [vp, u64p]),
     "mp_fsep_planner_next": (C.c_int, [vp, u8p]),
     "mp_fsep_planner_free": (None, [vp]),
+    "mp_fsep_plan_next": (C.c_int, [vp, u64p, u32, u32, u8p]),
     "mp_fsep_plan_layout": (C.c_int, [u32, u32, u32, C.c_double, C.c_double, C.c_double, C.c_double,
                                       u32, u64, u64p, u8p]),
     "mp_fsep_lite_routing": (C.c_int, [u32, u32, u64p, u8p, u64p]),

@@ -242,6 +242,23 @@ mp_status mp_fsep_planner_next(mp_fsep_planner* p, uint8_t* A_out) {
 
 void mp_fsep_planner_free(mp_fsep_planner* p) { delete p; }
 
+mp_status mp_fsep_plan_next(const mp_config* config, const uint64_t* R, uint32_t n_devices, uint32_t layer,
+                            uint8_t* A_out) {
+  return guarded([&] {
+    require(config && R && A_out, "mp_fsep_plan_next: NULL argument");
+    const RunConfig& c = config->cfg;
+    const Topology& topo = c.require_topology();
+    const CostParams& params = c.require_cost();
+    c.require_model();
+    c.require_seed();
+    require(topo.n_devices() == static_cast<int>(n_devices), "mp_fsep_plan_next: topology size != n_devices");
+    LayoutSearchSpec spec = c.search;
+    spec.seed = mix_seed(c.search.seed, 0x6c617972, layer);  // per-layer seed, as mp_plan_layer_json
+    const std::vector<RoutingMatrix> hist{matrix_from(R, n_devices, static_cast<uint32_t>(c.n_experts))};
+    layout_to(plan_layout(hist, topo, params, c.capacity, spec), A_out);
+  });
+}
+
 mp_status mp_fsep_plan_layout(uint32_t n_devices, uint32_t n_experts, uint32_t capacity, double bandwidth,
                               double v_comm, double v_comp, double b_comp, uint32_t epsilon, uint64_t seed,
                               const uint64_t* R, uint8_t* A_out) {

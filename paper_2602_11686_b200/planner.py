@@ -194,6 +194,15 @@ def trace_popularity(spec_json: str) -> np.ndarray:
     return out
 
 
+def plan_next(config: Config, R, layer: int = 0) -> np.ndarray:
+    """mp_fsep_plan_next: next-step layout of MoE layer `layer` from one observed R."""
+    R = _u64(R)
+    n, e = R.shape
+    A = np.zeros((e, n), dtype=np.uint8)
+    check(load().mp_fsep_plan_next(config._h, _p64(R), n, layer, _p8(A)))
+    return A
+
+
 class Planner:
     """Per-layer planner with history and the runtime's one-step lag
     (sim.cpp:99-149): next() is even_replication_layout before any observation,

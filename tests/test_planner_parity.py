@@ -160,3 +160,26 @@ def test_trace_export_replays_on_reference(product_lib, ref, tmp_path):
     from paper_2602_11686_b200._lib import MoeplanError
     with pytest.raises(MoeplanError):
         tr.append(0, 0, np.zeros((4, 8)))  # duplicate (iter, layer)
+
+
+def test_plan_next_matches_planner_handle_and_port(product_lib):
+    """mp_fsep_plan_next == a planner handle after one observation ==
+    the pinned port's plan_layout([R]) with the layer-salted seed, for several layers."""
+    rng = np.random.default_rng(11)
+    n, e, c = 8, 16, 4
+    cfg_json = json.dumps({"topology": {"n_nodes": 1, "devices_per_node": n, "b_intra": 9e11, "b_inter": 9e11},
+                           "cost": {"v_comm": 4096, "v_comp": 1.73e7, "b_comp": 1.6354e15},
+                           "model": {"n_experts": e, "capacity": c}, "planner": {"seed": 5, "epsilon": 4}})
+    cfg = PP.Config(cfg_json)
+    from oracle import planner_port as PORT
+    topo = PORT.Topology(1, n, 9e11, 9e11)
+    params = PORT.CostParams(4096, 1.73e7, 1.6354e15)
+    for layer in range(3):
+        R = rng.integers(0, 5000, size=(n, e))
+        A = PP.plan_next(cfg, R, layer)
+        h = PP.Planner(cfg, n, layer)
+        h.observe(R)
+        assert np.array_equal(A, h.next(e))
+        want = PORT.plan_layout([R.astype(np.int64).tolist()], topo, params, c,
+                                PORT.SearchSpec(4, PORT.mix_seed(5, 0x6C617972, layer)))
+        assert np.array_equal(A, np.array(want, dtype=np.uint8))

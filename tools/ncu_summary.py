@@ -50,7 +50,7 @@ def main():
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     name_i = hdr.index("Kernel Name")
-    lines, gemm_bytes = [], []
+    lines, gemm_bytes, gemm_pipe = [], [], []
     for r in data:
         full = r[name_i]
         short = full.split("(")[0].replace("void ", "").replace("fsep::", "").replace("(anonymous namespace)::", "")
@@ -75,6 +75,10 @@ def main():
             vals.append(f"{f:.4g}")
         if "grouped_gemm_pair_kernel" in full:
             gemm_bytes.append((rd + wr) * 1e9)
+            try:
+                gemm_pipe.append((float(vals[0]), float(vals[2])))  # (ms, tensor-pipe %)
+            except ValueError:
+                pass
         lines.append(" | ".join([label] + vals))
     with open(a.out, "w") as f:
         if a.header:
@@ -82,10 +86,14 @@ def main():
         f.write("# kernel | " + " | ".join(n for _, n in COLS) + "\n")
         f.write("\n".join(lines) + "\n")
     if a.traffic and gemm_bytes:
+        tot = sum(ms for ms, _ in gemm_pipe)
+        pipe = sum(ms * pct for ms, pct in gemm_pipe) / tot if tot else None
         json.dump({"dram_bytes_per_launch": sum(gemm_bytes) / len(gemm_bytes), "launches_averaged": len(gemm_bytes),
+                   "tensor_pipe_active_pct": round(pipe, 2) if pipe is not None else None,
                    "source": a.out,
                    "note": "mean dram__bytes_read.sum + dram__bytes_write.sum over the CTA-pair grouped-GEMM launches "
-                           "of one bench step (ncu --set full --clock-control none)"},
+                           "of one bench step (ncu --set full --clock-control none); tensor_pipe_active_pct: "
+                           "sm__pipe_tensor_cycles_active (pct of peak, elapsed) weighted by launch time"},
                   open(a.traffic, "w"), indent=1)
     print(f"{len(lines)} launches, {len(gemm_bytes)} pair-GEMM launches")
 
