@@ -267,8 +267,10 @@ def token_kernel_bandwidth(phases, layer, PL, N, rank, T, K, H, F=0, C=0):
     rms = phases.get("restore_landed_ms") or phases.get("restore_ms") or 0.0
     if N > 1 and F and C and rms > 0:
         b = C * 3 * H * F * 2 * (N - 1) // N
-        out["restore"] = {"ms": round(rms, 4), "bytes": b, "nvlink_GBps": round(b / (rms * 1e-3) / 1e9, 1),
-                          "note": "copy-engine pushes under the forward; restore begin -> last push landed"
+        out["restore"] = {"ms": round(rms, 4), "bytes": b, "effective_GBps_per_sending_gpu": round(b / (rms * 1e-3) / 1e9, 1),
+                          "note": "effective restore throughput of this (sending) GPU: its copy-engine pushes from the "
+                                  "restore's start to its last push landing (slots >= 1 are held back until dispatch "
+                                  "ends, so this is a lower bound on the link rate; raw rates: tools/transport_probe.py)"
                                   if phases.get("restore_landed_ms") else
                                   "copy-engine pushes under the forward; issue-to-join interval"}
     return out

@@ -1,0 +1,10 @@
+# end-of-round profile set (GPU box, 1 GPU): bench lines, ncu launch lists, one-step ncu --set full captures
+o=gpurun_out/r02f; mkdir -p $o
+python bench.py --steps 20 --warmup 5 > $o/mix.json 2> $o/mix.err; echo mix=$?
+python bench.py --config fine --steps 20 --warmup 5 > $o/fine.json 2> $o/fine.err; echo fine=$?
+python bench.py --config tiny --steps 20 --warmup 5 > $o/tiny.json 2> $o/tiny.err; echo tiny=$?
+python bench.py --config multilayer --steps 6 --warmup 3 --no-cpu > $o/ml.json 2> $o/ml.err; echo ml=$?
+for c in mixtral fine; do
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $o/launches_$c.csv python bench.py --config $c --steps 2 --warmup 3 --no-e2e --no-cpu > $o/ncul_$c.log 2>&1; echo ncul $c=$?
+  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"grouped_gemm|dispatch|combine|unpermute|router|plan_kernel|block_scan|expand" -s 40 -c 30 -o $o/full_$c python bench.py --config $c --steps 1 --warmup 3 --no-e2e --no-cpu > $o/ncuf_$c.log 2>&1; echo ncuf $c=$?
+done

@@ -10,4 +10,4 @@ for f in sys.argv[1:]:
     for k, v in (d.get("phases_ms_per_rank_layer0") or {}).items():
         print("  ", k, v)
     tk = d.get("token_kernels_layer0") or {}
-    print("  token kernels:", {k: (v["ms"], v.get("GBps"), v["nvlink_GBps"]) for k, v in tk.items()})
+    print("  token kernels:", {k: (v["ms"], v.get("GBps"), v.get("nvlink_GBps", v.get("effective_GBps_per_sending_gpu"))) for k, v in tk.items()})
