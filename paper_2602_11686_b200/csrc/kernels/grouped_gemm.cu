@@ -114,7 +114,8 @@ int env_raster(int kind) {
 }
 
 template <bool AMN, bool BMN, bool GK, int EPI>
-void launch_pair(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p, int grid, cudaStream_t st) {
+void launch_pair(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& b64, const GemmParams& p, int grid,
+                 cudaStream_t st) {
   auto kern = grouped_gemm_pair_kernel<AMN, BMN, GK, EPI>;
   static std::once_flag once;
   std::call_once(once, [&] {
@@ -132,7 +133,7 @@ void launch_pair(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, a, b, p);
+  cudaLaunchKernelEx(&cfg, kern, a, b, b64, p);
   count_launch();
 }
 }  // namespace
@@ -202,12 +203,20 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
     return v && std::string(v) == "cluster";
   }();
   if (rel_cluster) p.policy |= 0x400;
+  static const bool no_mtail = [] {  // FSEP_GEMM_MTAIL=0: masked M=256 tail tiles (A/B)
+    const char* v = std::getenv("FSEP_GEMM_MTAIL");
+    return v && std::string(v) == "0";
+  }();
+  if (no_mtail) p.policy |= 0x1000;
+  // the gate-up GEMM's M=128 tail tiles stage B as [gate 64 | up 64] halves (64-row box map)
+  const CUtensorMap& b64 = a.b64 != nullptr ? *a.b64 : tmB;
+  if (kind == GemmKind::kFwdGateUp && a.b64 != nullptr) p.policy |= 0x2000;
   switch (kind) {
-    case GemmKind::kFwdGateUp: launch_pair<false, false, false, kEpiSwigluFwd>(tmA, tmB, p, num_sms, stream); break;
-    case GemmKind::kFwdDown: launch_pair<false, false, false, kEpiBf16>(tmA, tmB, p, num_sms, stream); break;
-    case GemmKind::kBwdDownDgrad: launch_pair<false, true, false, kEpiSwigluBwd>(tmA, tmB, p, num_sms, stream); break;
-    case GemmKind::kBwdUpDgrad: launch_pair<false, true, false, kEpiBf16>(tmA, tmB, p, num_sms, stream); break;
-    case GemmKind::kBwdWgrad: launch_pair<true, true, true, kEpiF32>(tmA, tmB, p, num_sms, stream); break;
+    case GemmKind::kFwdGateUp: launch_pair<false, false, false, kEpiSwigluFwd>(tmA, tmB, b64, p, num_sms, stream); break;
+    case GemmKind::kFwdDown: launch_pair<false, false, false, kEpiBf16>(tmA, tmB, b64, p, num_sms, stream); break;
+    case GemmKind::kBwdDownDgrad: launch_pair<false, true, false, kEpiSwigluBwd>(tmA, tmB, b64, p, num_sms, stream); break;
+    case GemmKind::kBwdUpDgrad: launch_pair<false, true, false, kEpiBf16>(tmA, tmB, b64, p, num_sms, stream); break;
+    case GemmKind::kBwdWgrad: launch_pair<true, true, true, kEpiF32>(tmA, tmB, b64, p, num_sms, stream); break;
   }
 }
 

@@ -52,6 +52,8 @@ struct GemmParams {
                // bit 9: pair kernel uses a plain round-robin tile schedule (no snake / LPT group order)
                // bit 10: pair kernel releases the TMEM accumulator with a cluster-scope release (A/B)
                // bit 11: no wave synchronisation for this launch (A/B; launcher-side)
+               // bit 12: no M=128 tail tiles (masked M=256 tiles instead; A/B)
+               // bit 13: the launch has a 64-row-box B map (gate-up M=128 tail tiles)
   int raster;  // tile order within a group: 0 mode default, 1 m-inner, 2 n-inner, 3+ = m-chunks of `raster` tiles, n-inner
   // Optional per-group readiness (M-grouped only): before loading B of group g the
   // producer waits until ready[g * ready_n + q] has reached ready_epoch for all

@@ -14,8 +14,15 @@
 //   warps 2..9  epilogue: 8 warps = 4 TMEM lane quarters x 2 column halves
 //
 // Grouping modes and operand majorness are as in grouped_gemm.cuh.  M-grouped
-// segments are padded to 128 rows; a 256-row tile whose second half lies past
-// the segment is masked in the epilogue (those rows belong to the next segment).
+// segments are padded to 128 rows.  A group's last 256-row tile with only 128 rows
+// left runs as an M=128 pair MMA ("tail tile"): each CTA stages 64 rows of A and the
+// accumulator occupies N/2 TMEM columns -- lanes 0-63 hold rows 0-63 x columns
+// [0, N/2), lanes 64-127 the same rows x columns [N/2, N) (the cta_group::2, M=128
+// data-path layout) -- so no MMA work is spent on rows of the next segment.  For the
+// gate-up GEMM the tail tile's B is staged as [gate 0-63 | up 0-63] (CTA 0) and
+// [gate 64-127 | up 64-127] (CTA 1), so each lane still holds the gate and up
+// values of its features and SwiGLU stays fused.  (FSEP_GEMM_MTAIL=0 / policy
+// bit 12 falls back to the masked M=256 tile.)
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -133,7 +140,7 @@ __device__ __forceinline__ void pack_row64(const float* v, uint4 (&o)[4]) {
 template <bool kAMN, bool kBMN, bool kGroupK, int kEpi>
 __global__ void __launch_bounds__(gemm2::THREADS, 1)
     grouped_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                             const GemmParams p) {
+                             const __grid_constant__ CUtensorMap tmB64, const GemmParams p) {
   using namespace gemm2;
   using namespace fsep::ptx;
   extern __shared__ uint8_t smem_raw[];
@@ -218,6 +225,11 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
     raster_tile(local, mbs, nb, p.raster == 0 ? 16 : p.raster, kGroupK, mb, nbk);  // default: 16-tile m-chunks
   };
   auto k_blocks = [&](int g) { return kGroupK ? p.group_rows[g] / BK : p.K / BK; };
+  // M=128 tail tile: the group's last 256-row tile holds only 128 (padded) rows.  The
+  // gate-up GEMM needs the 64-row-box B map for its [gate|up] halves (policy bit 13).
+  const bool tails_ok = !kGroupK && EPI_WARPS == 8 && !(p.policy & 0x1000) &&
+                        (kEpi != kEpiSwigluFwd || (p.policy & 0x2000));
+  auto m_tail = [&](int g, int mb) { return tails_ok && p.group_rows[g] - mb * BM <= HALF; };
   // Tile of this CTA pair in wave w.  K-grouped: snake order (even waves ascending,
   // odd waves descending over the pairs), so consecutive waves hand the costlier
   // tiles of the descending-cost list to alternate ends -- LPT-like balance.
@@ -256,7 +268,10 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
           ready_g = g;
           FSEP_STALL_ADD(st_sync);
         }
-        const int m_half = mb * BM + rank * HALF;   // this CTA's first A row (M-grouped: within the group)
+        const bool mt = m_tail(g, mb);
+        // this CTA's first A row (M-grouped: within the group); a tail tile stages 64 rows per CTA
+        // (the 128-row box also brings the next 64 rows, which the M=128 MMA does not read)
+        const int m_half = mb * BM + rank * (mt ? HALF / 2 : HALF);
         // this CTA's first B column; a last N tile with <= 128 live columns runs as
         // UMMA N=128, each CTA providing 64 columns
         const bool n_tail = p.N - nbk * BN <= HALF && !(p.policy & 0x100);
@@ -278,7 +293,11 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
               tma_load_2d_pair(sA + i * 8192, &tmA, &full_bar[s], m_half + i * 64, row0 + kb * BK, pol_a);
           }
           if (!kGroupK) {
-            if (!kBMN) {
+            if (kEpi == kEpiSwigluFwd && mt) {  // [gate 64 | up 64] of this CTA's feature half
+              const int f0 = nbk * BN + rank * (HALF / 2);
+              tma_load_3d_pair(sB, &tmB64, &full_bar[s], kb * BK, f0, g, pol_b);
+              tma_load_3d_pair(sB + B_BYTES / 2, &tmB64, &full_bar[s], kb * BK, f0 + HALF, g, pol_b);
+            } else if (!kBMN) {
               tma_load_3d_pair(sB, &tmB, &full_bar[s], kb * BK, n_half, g, pol_b);
             } else {
 #pragma unroll
@@ -306,6 +325,8 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
     if (leader) {
       constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN, kAMN, kBMN);
       constexpr uint32_t idesc_tail = ptx::idesc_bf16(BM, BN / 2, kAMN, kBMN);  // last N tile with <= 128 columns
+      constexpr uint32_t idesc_m = ptx::idesc_bf16(HALF, BN, kAMN, kBMN);          // M=128 tail tile
+      constexpr uint32_t idesc_m_tail = ptx::idesc_bf16(HALF, BN / 2, kAMN, kBMN);  // M=128 and N=128
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
@@ -326,7 +347,8 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
         }
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + as * BN;
-        const uint32_t id = (p.N - nbk * BN <= HALF && !(p.policy & 0x100)) ? idesc_tail : idesc;
+        const bool ntl = p.N - nbk * BN <= HALF && !(p.policy & 0x100);
+        const uint32_t id = m_tail(g, mb) ? (ntl ? idesc_m_tail : idesc_m) : (ntl ? idesc_tail : idesc);
         for (int kb = 0; kb < nk; ++kb) {
           {
             FSEP_STALL_T0();
@@ -376,8 +398,17 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
       const int as = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       const int m_half = mb * BM + static_cast<int>(rank) * HALF;
-      const bool valid = kGroupK || m_half < p.group_rows[g];
-      if (kEpi == kEpiSwigluBwd && valid) {
+      // Tail tile (M=128 MMA): this CTA holds tile rows rank*64 + [0, 64); TMEM lanes 64-127
+      // repeat those rows for the upper half of the columns (see the file comment).
+      const bool mt = m_tail(g, mb);
+      const int tn = (p.N - nbk * BN <= HALF && !(p.policy & 0x100)) ? HALF : BN;  // MMA N of this tile
+      // first tile row of this warp's 32 lanes; TMEM columns [tc0, tc0 + tcw) of this warp;
+      // logical column of TMEM column tc = lc0 + (tc - tc0)
+      const int wrow0 = mt ? mb * BM + static_cast<int>(rank) * (HALF / 2) + static_cast<int>(quarter & 1) * 32
+                           : m_half + static_cast<int>(quarter) * 32;
+      const int tcw = mt ? tn / 4 : HALF;
+      const bool valid = kGroupK || mt || m_half < p.group_rows[g];
+      if (kEpi == kEpiSwigluBwd && valid && !mt) {
         // While the MMAs of this tile run, pull this row's h slice (one 128-feature
         // block: 256 contiguous bf16 = 512 B) into L2 so the epilogue loads hit L2.
         for (int half = half0; half < half0 + NHALF; ++half) {
@@ -402,6 +433,8 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
       if (valid)
 #pragma unroll 1
       for (int half = half0; half < half0 + NHALF; ++half) {
+        const int tc0 = half * tcw;                                                 // TMEM columns of this half
+        const int lc0 = mt ? static_cast<int>(quarter >> 1) * (tn / 2) + tc0 : tc0;  // their logical columns
         if (kEpi == kEpiF32) {
           // fp32 rows, stored coalesced: each 32-column chunk goes out as two 64-B row
           // pieces through the per-warp transpose tile (8 rows x 64 B per store)
@@ -432,23 +465,24 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
             }
           }
         } else if (kEpi == kEpiBf16) {
-          const long long row = p.group_off[g] + m_half + r;
+          const long long row = p.group_off[g] + wrow0 + static_cast<int>(lane);
           __nv_bfloat16* out = bf16_out_row(p, row);  // own row (row scatter resolved per lane)
 #ifndef FSEP_EPI_ROW64
           // 64-column passes, 128-B row pieces (fewer, larger remote writes for the row scatter)
           const uint32_t stg = ptx::smem_u32(smem + EPI_STAGE_OFF) + (warp - 2) * 4096;
 #pragma unroll 1
-          for (int j = 0; j < 2; ++j) {
-            const int c = half * 128 + j * 64;
-            const int col = nbk * BN + c;
+          for (int j = 0; j * 64 < tcw; ++j) {
+            const int tc = tc0 + j * 64;                 // TMEM column
+            const int col = nbk * BN + lc0 + j * 64;     // logical output column
             if (col >= p.N) break;
+            const int w = min(64, tcw - j * 64);         // 64, or 32 for an M=128 x N=128 tail tile
             float v[64];
-            tmem_ld32(taddr + c, *reinterpret_cast<float(*)[32]>(v));
-            if (col + 32 < p.N) tmem_ld32(taddr + c + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+            tmem_ld32(taddr + tc, *reinterpret_cast<float(*)[32]>(v));
+            if (w > 32 && col + 32 < p.N) tmem_ld32(taddr + tc + 32, *reinterpret_cast<float(*)[32]>(v + 32));
             uint4 o[8];
             pack_row64(v, *reinterpret_cast<uint4(*)[4]>(o));
             pack_row64(v + 32, *reinterpret_cast<uint4(*)[4]>(o + 4));
-            warp_store_rows128(stg, o, min(8, (p.N - col) / 8), [&](int rr) {
+            warp_store_rows128(stg, o, min(w / 8, (p.N - col) / 8), [&](int rr) {
               __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(
                   __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(out), rr));
               return d == nullptr ? d : d + col;
@@ -457,12 +491,11 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
 #else
           const uint32_t stg = ptx::smem_u32(smem + EPI_STAGE_OFF) + (warp - 2) * 2048;
 #pragma unroll 1
-          for (int j = 0; j < 4; ++j) {
-            const int c = half * 128 + j * 32;
-            const int col = nbk * BN + c;
+          for (int j = 0; j * 32 < tcw; ++j) {
+            const int col = nbk * BN + lc0 + j * 32;
             if (col >= p.N) break;
             float v[32];
-            tmem_ld32(taddr + c, v);
+            tmem_ld32(taddr + tc0 + j * 32, v);
             uint4 o[4];
             pack_row64(v, o);
             warp_store_rows64(stg, o, [&](int rr) {
@@ -475,15 +508,21 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
         } else if (kEpi == kEpiSwigluFwd) {
           // tile columns [0,128) = gate f0.., [128,256) = up f0..; this warp: f in [64*half, 64*half+64)
           const uint32_t stg = ptx::smem_u32(smem + EPI_STAGE_OFF) + (warp - 2) * 2048;
-          const long long row0 = p.group_off[g] + m_half + quarter * 32;
+          const long long row0 = p.group_off[g] + wrow0;
           __nv_bfloat16* hb = static_cast<__nv_bfloat16*>(p.out) + nbk * BN;
           __nv_bfloat16* ab = static_cast<__nv_bfloat16*>(p.out2) + nbk * (BN / 2);
+          // full tile: TMEM columns [0,128) gate, [128,256) up of the 128 features; this warp's
+          // features half*64 + [0,64).  Tail tile: TMEM [0,64) gate, [64,128) up of the features
+          // (quarter>>1)*64 + [0,64) (the [gate|up] B staging); this warp's 32 of them.
+          const int nf = mt ? 1 : 2;
 #pragma unroll 1
-          for (int j = 0; j < 2; ++j) {
-            const int f = half * 64 + j * 32;
+          for (int j = 0; j < nf; ++j) {
+            const int tg = mt ? half * 32 : half * 64 + j * 32;                      // TMEM column of the gates
+            const int tu = tg + (mt ? 64 : 128);                                    // ... of the ups
+            const int f = mt ? static_cast<int>(quarter >> 1) * 64 + half * 32 : tg;  // feature within the block
             float gv[32], uv[32];
-            tmem_ld32(taddr + f, gv);
-            tmem_ld32(taddr + 128 + f, uv);
+            tmem_ld32(taddr + tg, gv);
+            tmem_ld32(taddr + tu, uv);
             uint4 o[4];
             pack_row64(gv, o);
             warp_store_rows64(stg, o, [&](int rr) { return hb + (row0 + rr) * p.ldo + f; });
@@ -501,15 +540,15 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
           // than one 16-B piece of 32 different rows per instruction.  The h loads
           // of chunk j+1 are in flight while chunk j computes.
           const uint32_t stg = ptx::smem_u32(smem + EPI_STAGE_OFF) + (warp - 2) * 4096;
-          const long long row0 = p.group_off[g] + m_half + quarter * 32;
+          const long long row0 = p.group_off[g] + wrow0;
           const int sub = static_cast<int>(lane >> 2), cg = static_cast<int>(lane & 3);
           const __nv_bfloat16* hb = static_cast<const __nv_bfloat16*>(p.aux);
           __nv_bfloat16* db = static_cast<__nv_bfloat16*>(p.out);
           int nch = 0;
-          for (int j = 0; j < 4; ++j)
-            if (nbk * BN + half * 128 + j * 32 < p.N) nch = j + 1;
+          for (int j = 0; j * 32 < tcw; ++j)
+            if (nbk * BN + lc0 + j * 32 < p.N) nch = j + 1;
           auto hcol = [&](int j) {
-            const int f = nbk * BN + half * 128 + j * 32;
+            const int f = nbk * BN + lc0 + j * 32;
             return static_cast<long long>((f / 128) * 256 + (f % 128) + cg * 8);
           };
           auto load_h = [&](int j, uint4 (&gq)[4], uint4 (&uq)[4]) {
@@ -526,7 +565,7 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
 #pragma unroll 1
           for (int j = 0; j < nch; ++j) {
             float da[32];
-            tmem_ld32(taddr + half * 128 + j * 32, da);
+            tmem_ld32(taddr + tc0 + j * 32, da);
 #pragma unroll
             for (int q = 0; q < 8; ++q)
               sts128(stg + 16 * (lane * 8 + (q ^ (lane & 7))),

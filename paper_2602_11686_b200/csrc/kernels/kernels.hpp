@@ -41,6 +41,7 @@ struct GroupedGemmArgs {
   __nv_bfloat16* const* scatter = nullptr;
   long long scatter_rows = 0;
   int* wave_sync = nullptr;  // optional wave-synchronisation counters (see GemmParams), zeroed by the launcher
+  const CUtensorMap* b64 = nullptr;  // gate-up only: B map with 64-row boxes (M=128 tail tiles' [gate|up] staging)
 };
 
 enum class GemmKind : int {

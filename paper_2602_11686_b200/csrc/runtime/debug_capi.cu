@@ -42,6 +42,11 @@ __attribute__((visibility("default"))) mp_status mp_fsep_debug_grouped_gemm(
     if (wave_sync == nullptr && cudaMalloc(&wave_sync, kWaveSyncMax * sizeof(int)) != cudaSuccess)
       throw moeplan::Error(moeplan::ErrorKind::device, "cudaMalloc(wave_sync) failed");
     g.wave_sync = wave_sync;
+    CUtensorMap tb64{};
+    if (pair && k == GemmKind::kFwdGateUp) {  // M=128 tail tiles stage B as [gate 64 | up 64]
+      tb64 = make_tmap_3d(B, b_d0, b_d1, b_groups, b_pitch1, b_pitch2, 64, 64);
+      g.b64 = &tb64;
+    }
     if (pair)
       launch_grouped_gemm_pair(k, ta, tb, g, sms, static_cast<cudaStream_t>(stream));
     else

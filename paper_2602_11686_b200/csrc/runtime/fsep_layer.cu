@@ -115,6 +115,7 @@ struct Rank {
   PlanTables* pt = nullptr;
   int* wave_sync = nullptr;  // grouped-GEMM wave-synchronisation counters (FSEP_WAVE_SYNC=1)
   CUtensorMap tm_w13_k128{}, tm_w2_k128{};  // K-major weight maps with 128-row boxes (CTA-pair kernel)
+  CUtensorMap tm_w13_k64{};                  // ... 64-row boxes (gate-up M=128 tail tiles)
   CUtensorMap tm_x_k{}, tm_w13_k{}, tm_act_k{}, tm_w2_k{}, tm_dy_k{}, tm_w2_mn{}, tm_dh_k{}, tm_w13_mn{}, tm_dy_mn{},
       tm_act_mn{}, tm_dh_mn{}, tm_x_mn{};
   std::vector<Guard> guards;  // after every arena / private buffer
@@ -303,6 +304,7 @@ void build_maps(Layer& L, Rank& r) {
   r.tm_w13_k = make_tmap_3d(w13, H, 2 * F, C, H, L.flat, 64, 256);
   r.tm_w2_k = make_tmap_3d(w2, F, H, C, F, L.flat, 64, 256);
   r.tm_w13_k128 = make_tmap_3d(w13, H, 2 * F, C, H, L.flat, 64, 128);
+  r.tm_w13_k64 = make_tmap_3d(w13, H, 2 * F, C, H, L.flat, 64, 64);
   r.tm_w2_k128 = make_tmap_3d(w2, F, H, C, F, L.flat, 64, 128);
   r.tm_w2_mn = make_tmap_3d(w2, F, H, C, F, L.flat, 64, 64);
   r.tm_w13_mn = make_tmap_3d(w13, H, 2 * F, C, H, L.flat, 64, 64);
@@ -679,6 +681,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
     g.ldo = 2 * F;
     g.out2 = r.act;
     g.ldo2 = F;
+    g.b64 = &r.tm_w13_k64;
     gemm(L, GemmKind::kFwdGateUp, r.tm_x_k, r.tm_w13_k, r.tm_w13_k128, g, st);
     if (&r == &L.ranks.back()) {
       mark(L, st, kPhFwdGateUp);
