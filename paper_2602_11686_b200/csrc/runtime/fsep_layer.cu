@@ -208,6 +208,12 @@ extern "C" struct mp_fsep_layer {
   unsigned* err_host = nullptr;
   unsigned* err_dev = nullptr;
   unsigned long long spin_timeout_ns = 10000000000ull;  // FSEP_SPIN_TIMEOUT_MS (barriers, readiness waits)
+  // NCCL transport (FSEP_COMM=nccl, real mode): the restore as one grouped ncclSend /
+  // ncclRecv exchange on the side stream (the gate-up GEMM joins it as a whole), the
+  // reduce-scatter's chunks likewise into rs_stage, then the owner-side sum
+  bool nccl_mode = false;
+  ncclComm_t nccl = nullptr;
+  cudaEvent_t ev_nccl_rs = nullptr;
   // SM push transport (FSEP_COMM=sm): the same pushes and readiness flags as the copy
   // engines, issued by push_copies_kernel on the side stream (CopyTask batches in a ring)
   bool sm_push = false;
@@ -338,8 +344,8 @@ void allocate_rank(Layer& L, Rank& r) {
     if (push) {
       r.restored = ca.take<__nv_bfloat16>(C * flat, "restored");  // push target
       r.ready = ca.take<unsigned>(kMaxExperts * kMaxRanks, "ready");
-      r.rs_stage = ca.take<float>(E * N * S, "rs_stage");
     }
+    if (push || L.nccl_mode) r.rs_stage = ca.take<float>(E * N * S, "rs_stage");
   };
   auto carve_private = [&](Carver& cp) {
     if (multi) {
@@ -576,6 +582,61 @@ void push_restore(Layer& L, cudaStream_t st, int c0 = 0, int c1 = kMaxExperts) {
   }
 }
 
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw Error(ErrorKind::device, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+// NCCL transport: this rank's chunk of every expert hosted by d goes to d with ncclSend,
+// chunk p of every expert hosted here arrives from p with ncclRecv straight into its
+// restored slot (one group on the side stream, after `st`'s work; ev_restored after it).
+void nccl_restore(Layer& L, cudaStream_t st) {
+  const int E = L.E, N = L.N;
+  Rank& r = L.ranks[0];
+  CK(cudaEventRecord(L.ev_fork, st));
+  CK(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
+  mark(L, L.side, kPhRestoreBegin);
+  const std::vector<int> mine = hosted_experts(L.cur_layout, E, N, r.rank);
+  for (int c = 0; c < static_cast<int>(mine.size()); ++c)  // own chunk: local copy
+    CK(cudaMemcpyAsync(r.restored + static_cast<long long>(c) * L.flat + static_cast<long long>(r.rank) * L.S,
+                       r.shard + static_cast<long long>(mine[c]) * L.S, static_cast<size_t>(L.S) * 2,
+                       cudaMemcpyDeviceToDevice, L.side));
+  nccl_check(ncclGroupStart(), "ncclGroupStart");
+  for (int q = 1; q < N; ++q) {
+    const int d = (r.rank + q) % N, p = (r.rank + N - q) % N;
+    for (int e : hosted_experts(L.cur_layout, E, N, d))
+      nccl_check(ncclSend(r.shard + static_cast<long long>(e) * L.S, static_cast<size_t>(L.S), ncclBfloat16, d, L.nccl,
+                          L.side), "ncclSend");
+    for (int c = 0; c < static_cast<int>(mine.size()); ++c)
+      nccl_check(ncclRecv(r.restored + static_cast<long long>(c) * L.flat + static_cast<long long>(p) * L.S,
+                          static_cast<size_t>(L.S), ncclBfloat16, p, L.nccl, L.side), "ncclRecv");
+  }
+  nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  mark(L, L.side, kPhRestoreEnd);
+  CK(cudaEventRecord(L.ev_restored, L.side));
+}
+
+// NCCL reduce-scatter exchange: this rank's replica chunk o of every hosted expert to its
+// owner o; chunk `rank` of every expert from each of its other hosts into rs_stage.
+void nccl_grad_exchange(Layer& L, cudaStream_t st) {
+  const int E = L.E, N = L.N;
+  Rank& r = L.ranks[0];
+  CK(cudaEventRecord(L.ev_fork, st));
+  CK(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
+  const std::vector<int> mine = hosted_experts(L.cur_layout, E, N, r.rank);
+  nccl_check(ncclGroupStart(), "ncclGroupStart");
+  for (int q = 1; q < N; ++q) {
+    const int o = (r.rank + q) % N, p = (r.rank + N - q) % N;
+    for (int c = 0; c < static_cast<int>(mine.size()); ++c)
+      nccl_check(ncclSend(r.grad_full + static_cast<long long>(c) * L.flat + static_cast<long long>(o) * L.S,
+                          static_cast<size_t>(L.S), ncclFloat32, o, L.nccl, L.side), "ncclSend");
+    for (int e : hosted_experts(L.cur_layout, E, N, p))
+      nccl_check(ncclRecv(r.rs_stage + (static_cast<long long>(e) * N + p) * L.S, static_cast<size_t>(L.S),
+                          ncclFloat32, p, L.nccl, L.side), "ncclRecv");
+  }
+  nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  CK(cudaEventRecord(L.ev_nccl_rs, L.side));
+}
+
 void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __nv_bfloat16* y, cudaStream_t st) {
   if (T < 0 || T > L.T_max) throw Error(ErrorKind::invalid_argument, "forward: n_tokens exceeds max_tokens");
   const int E = L.E, K = L.K, H = L.H, F = L.F, N = L.N, C = L.C;
@@ -586,7 +647,7 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
   const bool ce = L.ce_mode;
   const bool prefetched = L.prefetched;  // chained: layout + restore already issued by the previous layer
   L.prefetched = false;
-  if (ce) {
+  if (ce || L.nccl_mode) {
     // Copy-engine restore needs the layout on the host: wait for the previous
     // step's planner callback (it ran right after that step's router, so the
     // host stays up to one step ahead) and snapshot it for this step.
@@ -608,6 +669,8 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
     // only slot 0 now; the other slots after dispatch, so the restore does not
     // compete with the dispatch for NVLink (slot 0 is what the GEMMs need first)
     if (!prefetched) push_restore(L, st, 0, L.restore_split ? 1 : kMaxExperts);
+  } else if (restore && L.nccl_mode) {
+    nccl_restore(L, st);
   } else if (restore) {
     CK(cudaEventRecord(L.ev_fork, st));
     CK(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
@@ -836,6 +899,8 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
     CK(cudaEventRecord(L.ev_w2, st));
     push_grads(L.ev_w2, w2_lo, L.flat);
   }
+  const bool nccl_rs = rs && L.nccl_mode;
+  if (nccl_rs) nccl_grad_exchange(L, st);  // under the dX GEMM (NCCL's CTAs get SMs as the GEMM frees them)
   for (Rank& r : L.ranks) {
     GroupedGemmArgs g2 = gemm_args(L, r);  // dX rows
     g2.N = H;
@@ -875,8 +940,13 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
                          st);
   }
   mark(L, st, kPhUnpermute);
-  if (rs && !ce_rs)
+  if (nccl_rs) {
+    CK(cudaStreamWaitEvent(st, L.ev_nccl_rs, 0));
+    for (Rank& r : L.ranks)
+      launch_grad_rs_sum(r.pt, r.grad_full, r.rs_stage, E, N, r.rank, L.S, L.flat, r.grad_shard, st);
+  } else if (rs && !ce_rs) {
     for (Rank& r : L.ranks) launch_grad_reduce_scatter(r.pt, L.peers, E, r.rank, L.S, L.flat, r.grad_shard, st);
+  }
   mark(L, st, kPhGradRS);
   if (deferred) join_rs(*deferred, st);  // long finished under this layer's GEMMs
   // join the planner stream (it finished long before the backward GEMMs did)
@@ -985,6 +1055,8 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     require(!(L->virt && (d.flags & MP_FSEP_FLAG_COPY_ENGINE)) || L->ce_mode || L->N == 1,
             "copy-engine mode unavailable (cuStreamWriteValue32 entry point missing)");
     L->sm_push = L->ce_mode && comm && std::string(comm) == "sm";
+    L->nccl_mode = !L->virt && L->N > 1 && comm && std::string(comm) == "nccl";
+    if (L->nccl_mode) L->ce_mode = false;
     // SM push: one push kernel per restore, launched at the forward's start (while the SMs
     // are free), so its CTAs are resident before the persistent gate-up GEMM polls the
     // flags.  A second kernel launched after dispatch could not always get CTAs beside the
@@ -1023,8 +1095,9 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     CK(cudaStreamCreateWithFlags(&L->side, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&L->plan_stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&L->cap_stream, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&L->ev_fork, &L->ev_restored, &L->ev_hist, &L->ev_planned, &L->ev_rs_done})
+    for (cudaEvent_t* e : {&L->ev_fork, &L->ev_restored, &L->ev_hist, &L->ev_planned, &L->ev_rs_done, &L->ev_nccl_rs})
       CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    if (L->nccl_mode) CK(cudaMallocHost(&L->layout_ring, 4 * static_cast<size_t>(L->E) * L->N));
     for (auto& ring : L->ev_g)
       for (auto& e : ring) CK(cudaEventCreate(&e));
     if (const char* v = std::getenv("FSEP_PHASE_TIMING"); v && std::string(v) == "1") {
@@ -1110,7 +1183,12 @@ void mp_fsep_layer_free(mp_fsep_layer* L) {
       for (auto e : L->ev_task) cudaEventDestroy(e);
     }
   }
-  for (cudaEvent_t e : {L->ev_fork, L->ev_restored, L->ev_hist, L->ev_planned, L->ev_rs_done}) cudaEventDestroy(e);
+  for (cudaEvent_t e : {L->ev_fork, L->ev_restored, L->ev_hist, L->ev_planned, L->ev_rs_done, L->ev_nccl_rs})
+    cudaEventDestroy(e);
+  if (L->nccl_mode) {
+    cudaFreeHost(L->layout_ring);
+    if (L->nccl) ncclCommDestroy(L->nccl);
+  }
   for (auto& ring : L->ev_g)
     for (auto e : ring) cudaEventDestroy(e);
   for (auto& ring : L->ev_p)
@@ -1141,7 +1219,7 @@ mp_status mp_fsep_layer_ipc_handle(mp_fsep_layer* L, void* out, size_t bytes) {
   });
 }
 
-mp_status mp_fsep_layer_connect(mp_fsep_layer* L, const void* all_handles, const void* /*nccl_id*/) {
+mp_status mp_fsep_layer_connect(mp_fsep_layer* L, const void* all_handles, const void* nccl_id) {
   return guarded([&] {
     require(L && all_handles, "mp_fsep_layer_connect: NULL argument");
     require(!L->virt, "connect is only used in real multi-GPU mode");
@@ -1184,6 +1262,12 @@ mp_status mp_fsep_layer_connect(mp_fsep_layer* L, const void* all_handles, const
     CK(cudaMemcpy(L->d_peer_flags, flags, sizeof(flags), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(L->d_peer_rs_flags, rs_flags, sizeof(rs_flags), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(L->d_tok_table, L->peers.tok_rows, sizeof(L->peers.tok_rows), cudaMemcpyHostToDevice));
+    if (L->nccl_mode) {  // FSEP_COMM=nccl: one communicator per layer (collective over the ranks)
+      require(nccl_id != nullptr, "mp_fsep_layer_connect: FSEP_COMM=nccl needs the NCCL unique id");
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      nccl_check(ncclCommInitRank(&L->nccl, L->N, id, L->ranks[0].rank), "ncclCommInitRank");
+    }
     L->connected = true;
   });
 }
@@ -1613,13 +1697,17 @@ mp_status mp_fsep_layer_graph_step(mp_fsep_layer* L, const void* x, const float*
       L->planner_pending = false;
       // A captured graph must not bake layout-dependent copy addresses: graphs use
       // the device-side (layout read on the GPU) restore / reduce-scatter kernels.
-      const bool ce_saved = L->ce_mode;
+      const bool ce_saved = L->ce_mode, nccl_saved = L->nccl_mode;
       L->ce_mode = false;
+      L->nccl_mode = false;
       struct Restore {
         mp_fsep_layer* l;
-        bool v;
-        ~Restore() { l->ce_mode = v; }
-      } restore_ce{L, ce_saved};
+        bool ce, nccl;
+        ~Restore() {
+          l->ce_mode = ce;
+          l->nccl_mode = nccl;
+        }
+      } restore_ce{L, ce_saved, nccl_saved};
       cudaStream_t cs = L->cap_stream;
       CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
       const uint64_t l0 = launches_issued();

@@ -79,18 +79,26 @@ class FsepLayer:
         check(self.lib.mp_fsep_layer_ipc_handle(self._h, buf, n))
         return bytes(buf)
 
-    def connect(self, handles: list[bytes]) -> None:
+    def connect(self, handles: list[bytes], nccl_id: Optional[bytes] = None) -> None:
         blob = b"".join(handles)
         buf = (C.c_char * len(blob)).from_buffer_copy(blob)
-        check(self.lib.mp_fsep_layer_connect(self._h, buf, None))
+        nid = (C.c_char * len(nccl_id)).from_buffer_copy(nccl_id) if nccl_id else None
+        check(self.lib.mp_fsep_layer_connect(self._h, buf, nid))
 
     def connect_torch_distributed(self) -> None:
-        """Exchange IPC handles with torch.distributed (any backend)."""
+        """Exchange IPC handles (and rank 0's NCCL unique id, used by the FSEP_COMM=nccl
+        transport) with torch.distributed (any backend)."""
         import torch.distributed as dist
         mine = self.ipc_handle()
         out = [None] * dist.get_world_size()
         dist.all_gather_object(out, mine)
-        self.connect(out)
+        nid = [None]
+        if dist.get_rank() == 0:
+            buf = (C.c_char * 128)()
+            check(self.lib.mp_fsep_nccl_unique_id(buf, 128))
+            nid[0] = bytes(buf)
+        dist.broadcast_object_list(nid, src=0)
+        self.connect(out, nid[0])
 
     # ------------------------------------------------------------ parameters
     def load_expert(self, e: int, w1: torch.Tensor, w3: torch.Tensor, w2: torch.Tensor, stream=None) -> None:

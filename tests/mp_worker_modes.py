@@ -11,7 +11,9 @@ one process per GPU, copy-engine communication).  Checks, in real multi-GPU mode
   the oracle's local-first variant bit for bit;
 * deferred gradient reduce-scatter (MP_FSEP_FLAG_DEFER_RS, PAPER Fig.5(e)): layer 2's
   reduce-scatter completed under layer 1's backward gives bit-identical gradients;
-* the SM push transport (FSEP_COMM=sm) is bit-identical to the copy engines;
+* the SM push transport (FSEP_COMM=sm) and the NCCL transport (FSEP_COMM=nccl:
+  grouped ncclSend/ncclRecv restore and gradient exchange) are bit-identical to the
+  copy engines;
 * no device-detected failure (barrier / readiness timeouts, overflow, memory guards).
 Exits non-zero on the first mismatch."""
 import json
@@ -106,8 +108,11 @@ def main():
     c = two_layer_steps(world, rank, chain=True, defer_rs=True)
     os.environ["FSEP_COMM"] = "sm"
     d = two_layer_steps(world, rank, chain=True)
+    os.environ["FSEP_COMM"] = "nccl"
+    n = two_layer_steps(world, rank, chain=True)
     del os.environ["FSEP_COMM"]
-    for tag, other in (("chained", b), ("deferred reduce-scatter", c), ("SM push transport", d)):
+    for tag, other in (("chained", b), ("deferred reduce-scatter", c), ("SM push transport", d),
+                       ("NCCL transport", n)):
         for step, (u, v) in enumerate(zip(a, other)):
             assert torch.equal(u[0], v[0]) and torch.equal(u[1], v[1]), f"{tag} outputs differ (step {step})"
             for gu, gv in zip(u[2], v[2]):
