@@ -458,7 +458,7 @@ void launch_tiled(const RouterArgs& a, int nblk, cudaStream_t st) {
 void launch_router(const RouterArgs& a, cudaStream_t st) {
   const int nblk = (a.T + kBlockTokens - 1) / kBlockTokens;
   if (nblk == 0) return;
-  if (a.E % 8 != 0 || a.E > kMaxExperts) throw std::runtime_error("router: n_experts must be a multiple of 8, <= 128");
+  if (a.E % 8 != 0 || a.E > kMaxExperts) throw std::runtime_error("router: n_experts must be a multiple of 8, <= 256");
   if (a.H % kHC != 0) throw std::runtime_error("router: hidden must be a multiple of 64");
   const size_t w_bytes = static_cast<size_t>(a.E) * a.H * sizeof(__nv_bfloat16);
   static bool attr = false;
@@ -497,6 +497,8 @@ void launch_router(const RouterArgs& a, cudaStream_t st) {
     }();
     if (tile == 8 && a.E % 8 == 0)
       launch_tiled<8, 8>(a, nblk, st);  // 8 x E/8 threads, 8x8 register tiles (half the smem traffic per FMA)
+    else if (a.E > 128)
+      launch_tiled<8, 4>(a, nblk, st);  // 8 x E/4 threads (<= 512 for E <= 256)
     else
       launch_tiled<4, 4>(a, nblk, st);  // 16 x E/4 threads
   }

@@ -694,10 +694,20 @@ __global__ void unpack_grad_kernel(const float* __restrict__ chunk, long long lo
   switch (CHV) {                                                                         \
     case 1: { constexpr int CH = 1; __VA_ARGS__; } break;                                \
     case 2: { constexpr int CH = 2; __VA_ARGS__; } break;                                \
+    case 3: { constexpr int CH = 3; __VA_ARGS__; } break;                                \
     case 4: { constexpr int CH = 4; __VA_ARGS__; } break;                                \
+    case 5: { constexpr int CH = 5; __VA_ARGS__; } break;                                \
+    case 6: { constexpr int CH = 6; __VA_ARGS__; } break;                                \
     case 8: { constexpr int CH = 8; __VA_ARGS__; } break;                                \
+    case 10: { constexpr int CH = 10; __VA_ARGS__; } break;                              \
+    case 12: { constexpr int CH = 12; __VA_ARGS__; } break;                              \
+    case 14: { constexpr int CH = 14; __VA_ARGS__; } break;                              \
     case 16: { constexpr int CH = 16; __VA_ARGS__; } break;                              \
-    default: throw std::runtime_error("hidden size must be 256 * {1,2,4,8,16}");         \
+    case 20: { constexpr int CH = 20; __VA_ARGS__; } break;                              \
+    case 24: { constexpr int CH = 24; __VA_ARGS__; } break;                              \
+    case 28: { constexpr int CH = 28; __VA_ARGS__; } break;                              \
+    case 32: { constexpr int CH = 32; __VA_ARGS__; } break;                              \
+    default: throw std::runtime_error("hidden size must be 256 * {1-6,8,10,12,14,16,20,24,28,32}"); \
   }
 
 void launch_block_scan(const int* blk_hist, int nblk, int E, int* blk_base, const PeerTable& peers, int rank,

@@ -1004,13 +1004,18 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     require(desc && out, "mp_fsep_layer_create: NULL argument");
     const mp_fsep_desc& d = *desc;
     require(d.world >= 1 && d.world <= static_cast<uint32_t>(kMaxRanks), "world must be in [1, 16]");
-    require(d.n_experts >= 1 && d.n_experts <= static_cast<uint32_t>(kMaxExperts), "n_experts must be in [1, 128]");
+    require(d.n_experts >= 1 && d.n_experts <= static_cast<uint32_t>(kMaxExperts), "n_experts must be in [1, 256]");
     require(d.top_k >= 1 && d.top_k <= 8 && d.top_k <= d.n_experts, "top_k must be in [1, min(8, E)]");
-    require(d.hidden % 256 == 0 && d.hidden >= 256 && d.hidden <= 4096, "hidden must be 256*{1,2,4,8,16}");
-    require((d.hidden & (d.hidden - 1)) == 0, "hidden must be 256*{1,2,4,8,16}");
+    // hidden = 256 * CH for the token kernels' row widths (routing.cu FSEP_CH_SWITCH): 256 ... 8192,
+    // e.g. 4096 (Mixtral), 2048, 5120, 6144, 7168 (DeepSeek-V3), 8192
+    static constexpr int kHiddenCh[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 14, 16, 20, 24, 28, 32};
+    require(d.hidden % 256 == 0 && std::find(std::begin(kHiddenCh), std::end(kHiddenCh),
+                                             static_cast<int>(d.hidden / 256)) != std::end(kHiddenCh),
+            "hidden must be 256 * {1-6, 8, 10, 12, 14, 16, 20, 24, 28, 32}");
     require(d.ffn % 128 == 0 && d.ffn > 0, "ffn must be a multiple of 128");
     require(d.capacity >= 1 && d.capacity <= d.n_experts && d.n_experts <= d.world * d.capacity,
             "capacity must satisfy 1 <= C <= E <= N*C");
+    require(d.capacity <= 128, "capacity (experts per device) must be <= 128 (grouped-GEMM group table)");
     require(d.top_k <= d.capacity * d.world, "top_k too large");
     require(d.virtual_ranks || d.rank < d.world, "rank out of range");
     const long long flat = 3LL * d.hidden * d.ffn;
