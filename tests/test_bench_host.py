@@ -66,7 +66,7 @@ def test_token_kernel_bytes_and_remote_rows():
     F, C = 512, 3
     rs = bench.token_kernel_bandwidth(dict(phases, restore_ms=2.0), _FakeLayer(R, A), PL, N, 0, T, K, H, F, C)
     assert rs["restore"]["bytes"] == C * 3 * H * F * 2 * (N - 1) // N
-    assert rs["restore"]["nvlink_GBps"] == round(rs["restore"]["bytes"] / 2e-3 / 1e9, 1)
+    assert rs["restore"]["effective_GBps_per_sending_gpu"] == round(rs["restore"]["bytes"] / 2e-3 / 1e9, 1)
 
 
 def test_calibrated_config_runs_reference_analysis():
