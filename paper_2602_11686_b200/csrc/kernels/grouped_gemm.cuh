@@ -137,7 +137,16 @@ constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*b
 
 // MUFU-based (approximate reciprocal, ~2 ulp fp32): the result is rounded to bf16, and an
 // IEEE division would cost a slow-path subroutine call per element in the epilogue.
+#ifdef FSEP_SIGMOID_TANH
+// A/B variant: one MUFU op (tanh.approx) instead of two (ex2 + rcp); absolute error ~2^-12.
+__device__ __forceinline__ float sigmoid_f(float g) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * g));
+  return fmaf(0.5f, t, 0.5f);
+}
+#else
 __device__ __forceinline__ float sigmoid_f(float g) { return __fdividef(1.0f, 1.0f + __expf(-g)); }
+#endif
 __device__ __forceinline__ float silu_f(float g) { return g * sigmoid_f(g); }
 
 __device__ __forceinline__ uint64_t pick_policy(int code, bool first_by_default) {
