@@ -185,7 +185,7 @@ class CpuReference:
         what = (f"all {self.sample} tokens of the {cfg_name} step ({self.N} simulated ranks, routed through "
                 f"lite_routing into the planned layout)" if self.full else
                 f"{self.sample} tokens of the {cfg_name} workload per step")
-        return (f"{what}: layer math via oracle/layer_oracle.py (numpy fp32, BLAS on {os.cpu_count()} cores) + "
+        return (f"{what}: layer math via oracle/layer_oracle.py (numpy fp32 BLAS, all host cores) + "
                 f"{planner}; measured per step, tokens/s = tokens / step seconds")
 
 
@@ -195,10 +195,23 @@ def cpu_sample_tokens(cfg, N, budget_flops):
     return max(64, min(2048, int(budget_flops / (18 * cfg["K"] * cfg["H"] * cfg["F"]))))
 
 
+def use_all_host_cores():
+    """torchrun sets OMP_NUM_THREADS=1 for every rank; the CPU reference path runs on rank 0
+    alone and should use every host core, so lift the BLAS thread limit at run time.
+    Returns the BLAS thread count in effect."""
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+        threadpool_limits(limits=os.cpu_count(), user_api="blas")
+        return max((i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"), default=1)
+    except Exception:
+        return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
+
+
 def run_reference_impl(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    threads = use_all_host_cores()
     N = cfg.get("virtual_ranks") or args.gpus
     C = args.capacity or cfg.get("capacity") or default_capacity(cfg["E"], cfg["K"], N)
     sample = args.cpu_sample or cpu_sample_tokens(cfg, N, 2.0e12)
@@ -211,8 +224,7 @@ def run_reference_impl(args, cfg):
             toks += n
             plan += ps
     rate = toks / sum(ts)
-    ncores = os.cpu_count()
-    cpu = {"value": rate, "unit": "tokens/s", "cores": ncores, "kind": "port", "sample": ref.describe(args.config),
+    cpu = {"value": rate, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": ref.describe(args.config),
            "planner_us_per_step": round(plan / len(ts) * 1e6, 2)}
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum(ts) / len(ts) * 1e3,
@@ -611,9 +623,10 @@ def main():
     # ---- CPU baseline (rank 0 at N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        threads = use_all_host_cores()
         ref = CpuReference(cfg, N, C, args.alpha, args.cpu_sample or cpu_sample_tokens(cfg, N, 2.0e12))
         sec, ntok, ps = ref.step()
-        cpu = {"value": ntok / sec, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+        cpu = {"value": ntok / sec, "unit": "tokens/s", "cores": threads, "kind": "port",
                "sample": ref.describe(args.config), "seconds": round(sec, 3),
                "planner_us_per_step": round(ps * 1e6, 2)}
 
