@@ -19,5 +19,7 @@ std::pair<std::string, std::string> simulate_artifacts(const RunConfig& config,
 std::vector<SchedulerKind> parse_scheduler_list(const std::string& csv);
 std::string analyze_json(const RunConfig& config);
 std::string stats_json(const std::vector<TraceRecord>& trace);
+// Greedy planner vs the exact optimum on one tiny instance (mp_oracle_gap_json).
+std::string oracle_gap_json(const RunConfig& config, const RoutingMatrix& instance);
 
 }  // namespace moeplan

@@ -57,6 +57,7 @@ def lib():
             "mp_plan_layer_json": (C.c_int, [vp, vp, u32, C.POINTER(vp)]),
             "mp_simulate": (C.c_int, [vp, vp, cp, C.POINTER(vp), C.POINTER(vp)]),
             "mp_analyze_json": (C.c_int, [vp, C.POINTER(vp)]),
+            "mp_oracle_gap_json": (C.c_int, [vp, cp, C.POINTER(vp)]),
         }
         for n, (r, a) in sigs.items():
             f = getattr(L, n)
@@ -120,6 +121,12 @@ def simulate(cfg: _Handle, trace: _Handle, schedulers: str):
     a, b = C.c_void_p(), C.c_void_p()
     _check(lib().mp_simulate(cfg.h, trace.h, schedulers.encode(), C.byref(a), C.byref(b)))
     return _take(a), _take(b)
+
+
+def oracle_gap_json(cfg: _Handle, instance_json: str) -> str:
+    out = C.c_void_p()
+    _check(lib().mp_oracle_gap_json(cfg.h, instance_json.encode(), C.byref(out)))
+    return _take(out)
 
 
 def analyze_json(cfg: _Handle) -> str:

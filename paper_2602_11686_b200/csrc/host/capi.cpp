@@ -199,9 +199,7 @@ mp_status mp_analyze_json(const mp_config* config, char** out_json) {
 mp_status mp_oracle_gap_json(const mp_config* config, const char* instance_json, char** out_json) {
   return guarded([&] {
     require(config && instance_json && out_json, "mp_oracle_gap_json: NULL argument");
-    throw Error(ErrorKind::invalid_argument,
-                "mp_oracle_gap_json: the exact brute-force solver is outside the B200 FSEP build "
-                "(use the reference moeplan for optimality-gap studies)");
+    *out_json = dup_string(oracle_gap_json(config->cfg, parse_instance(instance_json)));
   });
 }
 

@@ -134,6 +134,13 @@ def simulate(config: Config, trace: Trace, schedulers: str = "laer,static_ep"):
     return take_string(rj), take_string(rc)
 
 
+def oracle_gap_json(config: Config, instance_json: str) -> str:
+    """mp_oracle_gap_json: greedy planner vs the exact optimum on one tiny instance."""
+    p = C.c_void_p()
+    check(load().mp_oracle_gap_json(config._h, instance_json.encode(), C.byref(p)))
+    return take_string(p)
+
+
 def analyze_json(config: Config) -> str:
     p = C.c_void_p()
     check(load().mp_analyze_json(config._h, C.byref(p)))
