@@ -47,14 +47,27 @@ def test_status_names_and_last_error(product_lib):
     assert st == 2 and b"devices_per_node" in lib.mp_last_error()
 
 
-def test_oracle_gap_reports_scope(product_lib):
+def test_oracle_gap_status_and_output(product_lib):
+    """mp_oracle_gap_json follows the ABI conventions: a config without a topology is
+    invalid_argument (status 1) with the reason in mp_last_error; a complete config yields
+    the JSON report (exact optimum <= greedy cost)."""
     import ctypes as C
+    import json
     lib = product_lib
     cfg = C.c_void_p()
     assert lib.mp_config_parse(b'{"model": {"n_experts": 2, "capacity": 1}}', C.byref(cfg)) == 0
     out = C.c_void_p()
     assert lib.mp_oracle_gap_json(cfg, b'{"R": [[1, 2]]}', C.byref(out)) == 1
-    assert b"outside" in lib.mp_last_error()
+    assert b"topology" in lib.mp_last_error()
+    lib.mp_config_free(cfg)
+    full = json.dumps({"topology": {"n_nodes": 1, "devices_per_node": 2, "b_intra": 9e11, "b_inter": 9e11},
+                       "cost": {"v_comm": 8192, "v_comp": 3.5e8, "b_comp": 1.6e15},
+                       "model": {"n_experts": 2, "capacity": 1}, "planner": {"seed": 1}})
+    assert lib.mp_config_parse(full.encode(), C.byref(cfg)) == 0
+    assert lib.mp_oracle_gap_json(cfg, b'{"R": [[4, 2], [1, 3]]}', C.byref(out)) == 0
+    rep = json.loads(C.cast(out, C.c_char_p).value.decode())
+    lib.mp_string_free(out)
+    assert rep["exact_cost"] <= rep["greedy_cost"] and rep["gap"] >= 1.0 and rep["layouts_examined"] == 2
     lib.mp_config_free(cfg)
 
 
