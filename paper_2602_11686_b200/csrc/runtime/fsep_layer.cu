@@ -792,6 +792,13 @@ void run_forward(Layer& L, const __nv_bfloat16* x, const float* bias, int T, __n
 void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStream_t st) {
   const int E = L.E, K = L.K, H = L.H, F = L.F, N = L.N, T = L.T_step;
   const long long TH = static_cast<long long>(T) * H;
+  // This layer's own reduce-scatter of the previous step still pending (its predecessor's
+  // backward never ran): complete it before this backward overwrites grad_full.
+  if (L.rs_state != 0) {
+    CK(cudaEventRecord(L.ev_fork, st));
+    CK(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
+    join_rs(L, st);
+  }
   // Fig.5(e): the next layer (already back-propagated this step) deferred the owner-side
   // half of its reduce-scatter; it runs on that layer's side stream under this layer's GEMMs.
   Layer* deferred = (L.next && L.next->rs_state == 1) ? L.next : nullptr;
