@@ -21,7 +21,9 @@ constexpr int kMaxRanks = 16;
 constexpr int kMaxExperts = 256;  // DeepSeek-V3-class layers (E = 256)
 constexpr int kWaveSyncMax = 4096;  // wave-synchronisation counters per grouped-GEMM launch
 constexpr int kBlockTokens = 64;  // router / ranking tile (8 warps x 8 tokens)
-constexpr int kDLCols = 256;      // width of the dense router-gradient matrix dL[t][e] (>= E)
+constexpr int kDLCols = 256;      // max width of the dense router-gradient matrix dL[t][e] (>= E)
+// its width for E experts: 128 (one single-CTA M tile) up to 128 experts, else 256
+__host__ __device__ constexpr int dl_cols(int E) { return E <= 128 ? 128 : 256; }
 constexpr int kRouterWgradChunk = 1024;  // token rows per split-K group of the router wgrad GEMM
 
 // Token-slot rows: every rank owns tok_rows[T_max * K][H] indexed by its own

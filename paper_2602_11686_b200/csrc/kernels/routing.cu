@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(int T, int K, const __
                                                           const __nv_bfloat16* __restrict__ tok_rows,
                                                           const uint32_t* __restrict__ slot_dst, PeerTable peers,
                                                           float* __restrict__ dl, __nv_bfloat16* __restrict__ dl_dense,
-                                                          int* __restrict__ rw_rows, int* __restrict__ rw_off,
+                                                          int* __restrict__ rw_rows, int* __restrict__ rw_off, int dlc,
                                                           int src_rank, int T_max, bool dedupe) {
   constexpr int H = CH * 256;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(int T, int K, const __
     for (int k = 0; k < K; ++k) {
       const float v = w[k] * (dw[k] - mix);
       dl[static_cast<size_t>(t) * K + k] = v;
-      dl_dense[static_cast<size_t>(t) * kDLCols + topk_idx[static_cast<size_t>(t) * K + k]] = __float2bfloat16_rn(v);
+      dl_dense[static_cast<size_t>(t) * dlc + topk_idx[static_cast<size_t>(t) * K + k]] = __float2bfloat16_rn(v);
     }
 }
 
@@ -544,12 +544,12 @@ __global__ void __launch_bounds__(256) unpermute_bwd_kernel(int T, int K, const 
 // dWg = dL^T x runs as a split-K tcgen05 GEMM (K-grouped over token chunks, one
 // [kDLCols x H] fp32 partial per chunk); the partials' first E rows are summed
 // here in fixed chunk order (deterministic).
-__global__ void router_wgrad_reduce_kernel(const float* __restrict__ partial, int splits, int EH, int H,
+__global__ void router_wgrad_reduce_kernel(const float* __restrict__ partial, int splits, int EH, int H, int dlc,
                                            float* __restrict__ dwg) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= EH) return;
   float s = 0.f;
-  for (int p = 0; p < splits; ++p) s += partial[static_cast<size_t>(p) * kDLCols * H + i];
+  for (int p = 0; p < splits; ++p) s += partial[static_cast<size_t>(p) * dlc * H + i];
   dwg[i] = s;
 }
 
@@ -769,16 +769,17 @@ void launch_combine(int T, int H, int K, const float* topk_w, const __nv_bfloat1
   count_launch();
 }
 
-void launch_combine_bwd(int T, int H, int K, const __nv_bfloat16* dout, const float* topk_w, const int* topk_idx,
+void launch_combine_bwd(int T, int H, int K, int E, const __nv_bfloat16* dout, const float* topk_w, const int* topk_idx,
                         const __nv_bfloat16* tok_rows, const uint32_t* slot_dst, const PeerTable& peers, float* dl,
                         __nv_bfloat16* dl_dense, int* rw_rows, int* rw_off, int rank, int T_max, bool dedupe,
                         cudaStream_t st) {
   if (T == 0) return;
   const size_t tpad = (static_cast<size_t>(T) + 127) / 128 * 128;
-  cudaMemsetAsync(dl_dense, 0, tpad * kDLCols * sizeof(__nv_bfloat16), st);
+  const int dlc = dl_cols(E);
+  cudaMemsetAsync(dl_dense, 0, tpad * dlc * sizeof(__nv_bfloat16), st);
   FSEP_CH_SWITCH(H / 256, combine_bwd_kernel<CH><<<(T + 7) / 8, 256, 0, st>>>(
                               T, K, dout, topk_w, topk_idx, tok_rows, slot_dst, peers, dl, dl_dense, rw_rows, rw_off,
-                              rank, T_max, dedupe));
+                              dlc, rank, T_max, dedupe));
   count_launch();
 }
 
@@ -806,25 +807,26 @@ void launch_router_wgrad(const __nv_bfloat16* x, int T, int H, int E, const __nv
                          const int* rw_rows, const int* rw_off, float* partial, float* dwg, int num_sms,
                          cudaStream_t st) {
   const int splits = router_wgrad_splits(T);
+  const int dlc = dl_cols(E);
   if (T > 0) {
     // dL [rows][kDLCols] and x [rows][H] are both MN-major operands of the K-grouped GEMM
     const uint64_t tmax_pad = (static_cast<uint64_t>(T_max) + 127) / 128 * 128;
-    const CUtensorMap ta = make_tmap_2d(dl_dense, kDLCols, tmax_pad, kDLCols, 64, 64);
+    const CUtensorMap ta = make_tmap_2d(dl_dense, dlc, tmax_pad, dlc, 64, 64);
     const CUtensorMap tb = make_tmap_2d(x, H, static_cast<uint64_t>(T), H, 64, 64);
     GroupedGemmArgs g{};
     g.num_groups = splits;
     g.group_rows = rw_rows;
     g.group_off = rw_off;
-    g.M = kDLCols;
+    g.M = dlc;
     g.N = H;
     g.out = partial;
     g.ldo = H;
-    g.out_group_stride = static_cast<long long>(kDLCols) * H;
+    g.out_group_stride = static_cast<long long>(dlc) * H;
     launch_grouped_gemm(GemmKind::kBwdWgrad, ta, tb, g, num_sms, st);
   } else {
-    cudaMemsetAsync(partial, 0, static_cast<size_t>(kDLCols) * H * sizeof(float), st);
+    cudaMemsetAsync(partial, 0, static_cast<size_t>(dlc) * H * sizeof(float), st);
   }
-  router_wgrad_reduce_kernel<<<(E * H + 255) / 256, 256, 0, st>>>(partial, splits, E * H, H, dwg);
+  router_wgrad_reduce_kernel<<<(E * H + 255) / 256, 256, 0, st>>>(partial, splits, E * H, H, dlc, dwg);
   count_launch();
 }
 

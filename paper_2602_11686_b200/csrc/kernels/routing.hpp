@@ -45,7 +45,7 @@ void launch_zero_pad(const PlanTables* pt, int C, int H, __nv_bfloat16* x_rows, 
 void launch_dispatch(const DispatchArgs& a, cudaStream_t st);
 void launch_combine(int T, int H, int K, const float* topk_w, const __nv_bfloat16* tok_rows, __nv_bfloat16* out,
                     cudaStream_t st);
-void launch_combine_bwd(int T, int H, int K, const __nv_bfloat16* dout, const float* topk_w, const int* topk_idx,
+void launch_combine_bwd(int T, int H, int K, int E, const __nv_bfloat16* dout, const float* topk_w, const int* topk_idx,
                         const __nv_bfloat16* tok_rows, const uint32_t* slot_dst, const PeerTable& peers, float* dl,
                         __nv_bfloat16* dl_dense, int* rw_rows, int* rw_off, int rank, int T_max, bool dedupe,
                         cudaStream_t st);

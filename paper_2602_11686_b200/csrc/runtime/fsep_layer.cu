@@ -809,7 +809,7 @@ void run_backward(Layer& L, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStre
   }
   for (size_t v = 0; v < L.ranks.size(); ++v) {
     Rank& r = L.ranks[v];
-    launch_combine_bwd(T, H, K, dy + (L.virt ? static_cast<long long>(v) * TH : 0), r.topk_w, r.topk_idx, r.tok_rows,
+    launch_combine_bwd(T, H, K, E, dy + (L.virt ? static_cast<long long>(v) * TH : 0), r.topk_w, r.topk_idx, r.tok_rows,
                        r.slot_dst, L.peers, r.dl, r.dl_dense, r.rw_rows, r.rw_off, r.rank, L.T_max, L.dedupe, st);
     launch_router_wgrad(r.x_in, T, H, E, r.dl_dense, L.T_max, r.rw_rows, r.rw_off, r.dwg_partial, r.dwg, L.num_sms,
                         st);
