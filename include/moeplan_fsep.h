@@ -156,6 +156,10 @@ size_t mp_fsep_ipc_bytes(void);
 mp_status mp_fsep_nccl_unique_id(void* out, size_t bytes);
 mp_status mp_fsep_layer_ipc_handle(mp_fsep_layer* layer, void* out, size_t bytes);
 mp_status mp_fsep_layer_connect(mp_fsep_layer* layer, const void* all_handles, const void* nccl_id);
+/* One process driving all N GPUs (tools, profiling): connect real-mode layers
+ * layers[i] = rank i (each created on its own device) through direct peer access
+ * instead of CUDA IPC. */
+mp_status mp_fsep_layer_connect_local(mp_fsep_layer** layers, uint32_t n);
 
 /* Parameters.  Weights are given unfused and unsharded (device or pinned host
  * pointers); each rank keeps its 1/N FSEP shard of every expert.  vrank

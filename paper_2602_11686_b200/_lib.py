@@ -84,6 +84,7 @@ _SIGS = {
     "mp_fsep_nccl_unique_id": (C.c_int, [vp, C.c_size_t]),
     "mp_fsep_layer_ipc_handle": (C.c_int, [vp, vp, C.c_size_t]),
     "mp_fsep_layer_connect": (C.c_int, [vp, vp, vp]),
+    "mp_fsep_layer_connect_local": (C.c_int, [C.POINTER(vp), u32]),
     "mp_fsep_layer_load_expert": (C.c_int, [vp, u32, vp, vp, vp, vp]),
     "mp_fsep_layer_load_router": (C.c_int, [vp, vp, vp]),
     "mp_fsep_layer_set_layout": (C.c_int, [vp, u8p]),

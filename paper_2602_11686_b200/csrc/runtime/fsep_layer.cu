@@ -1231,49 +1231,63 @@ mp_status mp_fsep_layer_ipc_handle(mp_fsep_layer* L, void* out, size_t bytes) {
   });
 }
 
+}  // extern "C"
+
+namespace {
+// Fills L's peer tables from every rank's arena base address (as mapped in this
+// process); identical carving on every rank gives identical offsets.
+void connect_bases(mp_fsep_layer* L, const std::vector<char*>& bases) {
+  Rank& me = L->ranks[0];
+  unsigned int* flags[kMaxRanks] = {};
+  unsigned int* rs_flags[kMaxRanks] = {};
+  auto off = [&](const void* q) { return static_cast<const char*>(q) - static_cast<char*>(me.arena); };
+  for (int p = 0; p < L->N; ++p) {
+    char* base = bases[static_cast<size_t>(p)];
+    L->peers.x_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.x_rows));
+    L->peers.dy_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.dy_rows));
+    L->peers.tok_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.tok_rows));
+    L->peers.row_src[p] = reinterpret_cast<int*>(base + off(me.row_src));
+    if (L->dedupe) {
+      L->peers.stage[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.stage));
+      L->peers.row_w[p] = reinterpret_cast<float*>(base + off(me.row_w));
+    }
+    if (L->ce_mode) {
+      L->peer_restored[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.restored));
+      L->peer_ready[p] = reinterpret_cast<unsigned*>(base + off(me.ready));
+      L->peer_rs_stage[p] = reinterpret_cast<float*>(base + off(me.rs_stage));
+    }
+    L->peers.R_all[p] = reinterpret_cast<unsigned long long*>(base + off(me.R_all));
+    L->peers.grad_full[p] = reinterpret_cast<float*>(base + off(me.grad_full));
+    L->peers.shard[p] = reinterpret_cast<const __nv_bfloat16*>(base + off(me.shard));
+    flags[p] = reinterpret_cast<unsigned int*>(base + off(me.flags));
+    rs_flags[p] = reinterpret_cast<unsigned int*>(base + off(me.rs_flags));
+  }
+  CK(cudaMemcpy(L->d_peer_flags, flags, sizeof(flags), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(L->d_peer_rs_flags, rs_flags, sizeof(rs_flags), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(L->d_tok_table, L->peers.tok_rows, sizeof(L->peers.tok_rows), cudaMemcpyHostToDevice));
+}
+}  // namespace
+
+extern "C" {
+
 mp_status mp_fsep_layer_connect(mp_fsep_layer* L, const void* all_handles, const void* nccl_id) {
   return guarded([&] {
     require(L && all_handles, "mp_fsep_layer_connect: NULL argument");
     require(!L->virt, "connect is only used in real multi-GPU mode");
     CK(cudaSetDevice(L->device));
     const auto* hs = static_cast<const cudaIpcMemHandle_t*>(all_handles);
-    Rank& me = L->ranks[0];
-    unsigned int* flags[kMaxRanks] = {};
-    unsigned int* rs_flags[kMaxRanks] = {};
+    std::vector<char*> bases(static_cast<size_t>(L->N));
     for (int p = 0; p < L->N; ++p) {
-      char* base;
-      if (p == me.rank) {
-        base = static_cast<char*>(me.arena);
+      if (p == L->ranks[0].rank) {
+        bases[static_cast<size_t>(p)] = static_cast<char*>(L->ranks[0].arena);
       } else {
         void* ptr = nullptr;
         CK(cudaIpcOpenMemHandle(&ptr, hs[p], cudaIpcMemLazyEnablePeerAccess));
         L->opened_ptrs.push_back(ptr);
-        base = static_cast<char*>(ptr);
+        bases[static_cast<size_t>(p)] = static_cast<char*>(ptr);
       }
-      // identical carving on every rank -> identical offsets
-      auto off = [&](const void* q) { return static_cast<const char*>(q) - static_cast<char*>(me.arena); };
-      L->peers.x_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.x_rows));
-      L->peers.dy_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.dy_rows));
-      L->peers.tok_rows[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.tok_rows));
-      L->peers.row_src[p] = reinterpret_cast<int*>(base + off(me.row_src));
-      if (L->dedupe) {
-        L->peers.stage[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.stage));
-        L->peers.row_w[p] = reinterpret_cast<float*>(base + off(me.row_w));
-      }
-      if (L->ce_mode) {
-        L->peer_restored[p] = reinterpret_cast<__nv_bfloat16*>(base + off(me.restored));
-        L->peer_ready[p] = reinterpret_cast<unsigned*>(base + off(me.ready));
-        L->peer_rs_stage[p] = reinterpret_cast<float*>(base + off(me.rs_stage));
-      }
-      L->peers.R_all[p] = reinterpret_cast<unsigned long long*>(base + off(me.R_all));
-      L->peers.grad_full[p] = reinterpret_cast<float*>(base + off(me.grad_full));
-      L->peers.shard[p] = reinterpret_cast<const __nv_bfloat16*>(base + off(me.shard));
-      flags[p] = reinterpret_cast<unsigned int*>(base + off(me.flags));
-      rs_flags[p] = reinterpret_cast<unsigned int*>(base + off(me.rs_flags));
     }
-    CK(cudaMemcpy(L->d_peer_flags, flags, sizeof(flags), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(L->d_peer_rs_flags, rs_flags, sizeof(rs_flags), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(L->d_tok_table, L->peers.tok_rows, sizeof(L->peers.tok_rows), cudaMemcpyHostToDevice));
+    connect_bases(L, bases);
     if (L->nccl_mode) {  // FSEP_COMM=nccl: one communicator per layer (collective over the ranks)
       require(nccl_id != nullptr, "mp_fsep_layer_connect: FSEP_COMM=nccl needs the NCCL unique id");
       ncclUniqueId id;
@@ -1281,6 +1295,30 @@ mp_status mp_fsep_layer_connect(mp_fsep_layer* L, const void* all_handles, const
       nccl_check(ncclCommInitRank(&L->nccl, L->N, id, L->ranks[0].rank), "ncclCommInitRank");
     }
     L->connected = true;
+  });
+}
+
+mp_status mp_fsep_layer_connect_local(mp_fsep_layer** layers, uint32_t n) {
+  return guarded([&] {
+    require(layers && n >= 1, "mp_fsep_layer_connect_local: bad argument");
+    for (uint32_t i = 0; i < n; ++i) {
+      require(layers[i] && !layers[i]->virt && layers[i]->N == static_cast<int>(n) &&
+                  layers[i]->ranks[0].rank == static_cast<int>(i) && !layers[i]->nccl_mode,
+              "mp_fsep_layer_connect_local: layers[i] must be real-mode rank i of an n-rank layer");
+    }
+    std::vector<char*> bases(n);
+    for (uint32_t i = 0; i < n; ++i) bases[i] = static_cast<char*>(layers[i]->ranks[0].arena);
+    for (uint32_t i = 0; i < n; ++i) {
+      CK(cudaSetDevice(layers[i]->device));
+      for (uint32_t j = 0; j < n; ++j) {
+        if (layers[j]->device == layers[i]->device) continue;
+        const cudaError_t e = cudaDeviceEnablePeerAccess(layers[j]->device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else CK(e);
+      }
+      connect_bases(layers[i], bases);
+      layers[i]->connected = true;
+    }
   });
 }
 
