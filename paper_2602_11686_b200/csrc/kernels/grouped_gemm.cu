@@ -6,6 +6,8 @@
 
 #include <atomic>
 #include <mutex>
+#include <set>
+#include <utility>
 #include <stdexcept>
 #include <string>
 
@@ -38,6 +40,15 @@ void check_encode(CUresult r, const char* what) {
 }  // namespace
 
 uint64_t launches_issued() { return g_launches.load(); }
+
+void set_smem_attr(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.insert({func, dev}).second) cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
 
 bool gemm_stall_counters(unsigned long long* out, bool reset) {
 #ifdef FSEP_GEMM_STALLS
@@ -96,10 +107,7 @@ namespace {
 template <bool AMN, bool BMN, bool GK, int EPI>
 void launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p, int grid, cudaStream_t st) {
   auto kern = grouped_gemm_kernel<AMN, BMN, GK, EPI>;
-  static std::once_flag once;
-  std::call_once(once, [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::SMEM_BYTES);
-  });
+  set_smem_attr(reinterpret_cast<const void*>(kern), gemm::SMEM_BYTES);
   kern<<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(a, b, p);
   count_launch();
 }
@@ -117,10 +125,7 @@ template <bool AMN, bool BMN, bool GK, int EPI>
 void launch_pair(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& b64, const GemmParams& p, int grid,
                  cudaStream_t st) {
   auto kern = grouped_gemm_pair_kernel<AMN, BMN, GK, EPI>;
-  static std::once_flag once;
-  std::call_once(once, [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm2::smem_bytes(EPI));
-  });
+  set_smem_attr(reinterpret_cast<const void*>(kern), gemm2::smem_bytes(EPI));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(grid & ~1));
   cfg.blockDim = dim3(gemm2::THREADS);

@@ -60,6 +60,11 @@ bool pair_gemm_supported(GemmKind kind, const GroupedGemmArgs& args);
 void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUtensorMap& tmB,
                               const GroupedGemmArgs& args, int num_sms, cudaStream_t stream);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, current device):
+// function attributes belong to each device's context, so a process driving several
+// GPUs must set them on every device it launches on.
+void set_smem_attr(const void* func, int bytes);
+
 // Kernel-count bookkeeping for bench/roofline (launches issued by this library).
 uint64_t launches_issued();
 // Dev builds (-DFSEP_GEMM_STALLS): per-role barrier-wait cycle totals of the pair

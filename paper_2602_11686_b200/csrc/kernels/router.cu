@@ -444,11 +444,7 @@ template <int TT, int TE>
 void launch_tiled(const RouterArgs& a, int nblk, cudaStream_t st) {
   const int threads = (kBlockTokens / TT) * (a.E / TE);
   const size_t smem = static_cast<size_t>(kHC) * (kBlockTokens + a.E) * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(router_gemm_kernel<TT, TE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    attr = true;
-  }
+  set_smem_attr(reinterpret_cast<const void*>(router_gemm_kernel<TT, TE>), 96 * 1024);
   router_gemm_kernel<TT, TE><<<nblk, threads, smem, st>>>(a.x, a.wg, a.bias, a.T, a.H, a.E, a.K, a.topk_idx,
                                                           a.topk_w, a.intra_rank, a.blk_hist);
 }
@@ -461,22 +457,14 @@ void launch_router(const RouterArgs& a, cudaStream_t st) {
   if (a.E % 8 != 0 || a.E > kMaxExperts) throw std::runtime_error("router: n_experts must be a multiple of 8, <= 256");
   if (a.H % kHC != 0) throw std::runtime_error("router: hidden must be a multiple of 64");
   const size_t w_bytes = static_cast<size_t>(a.E) * a.H * sizeof(__nv_bfloat16);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(router_small_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(router_small_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  set_smem_attr(reinterpret_cast<const void*>(router_small_kernel<8>), 200 * 1024);
+  set_smem_attr(reinterpret_cast<const void*>(router_small_kernel<16>), 200 * 1024);
   static const bool small = [] {
     const char* v = std::getenv("FSEP_ROUTER");
     return v && std::string(v) == "small";
   }();
-  static bool attr2 = false;
-  if (!attr2) {
-    cudaFuncSetAttribute(router_pair_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(router_pair_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr2 = true;
-  }
+  set_smem_attr(reinterpret_cast<const void*>(router_pair_kernel<8>), 200 * 1024);
+  set_smem_attr(reinterpret_cast<const void*>(router_pair_kernel<16>), 200 * 1024);
   if (!small && a.E == 8 && w_bytes <= 200 * 1024)
     router_pair_kernel<8><<<nblk, kBlockTokens * 4, w_bytes, st>>>(a.x, a.wg, a.bias, a.T, a.H, a.K, a.topk_idx,
                                                                    a.topk_w, a.intra_rank, a.blk_hist);

@@ -743,12 +743,7 @@ void launch_dispatch(const DispatchArgs& a, cudaStream_t st) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     FSEP_CH_SWITCH(a.H / 256, {
       constexpr size_t smem = dispatch_smem<CH>() + kDispatchWarps * dispatch_bufs<CH>() * 8;
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(dispatch_tma_kernel<CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        attr = true;
-      }
+      set_smem_attr(reinterpret_cast<const void*>(dispatch_tma_kernel<CH>), static_cast<int>(smem));
       const int blocks = std::min(sms, (a.T + kDispatchWarps - 1) / kDispatchWarps);
       dispatch_tma_kernel<CH><<<blocks, kDispatchWarps * 32, smem, st>>>(
           a.x, a.T, a.K, a.E, a.topk_idx, a.intra_rank, a.blk_base, a.pt, a.peers, a.slot_dst, a.rank, a.topk_w,
