@@ -13,8 +13,14 @@ reported, ignored here); the data movement of each profiled kernel is unchanged.
 Without ncu the probe checks the step is healthy (no device-detected failure).
 usage: python tools/nvlink_ncu_probe.py {mixtral|fine} N [steps]"""
 import ctypes as C
+import os
 import sys
 from pathlib import Path
+
+# One host thread drives every GPU: with lazy module loading the first launch of a kernel
+# on a device waits for that device to go idle, which a cross-GPU barrier kernel waiting
+# for a not-yet-launched peer never does -- load every module up front instead.
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 import numpy as np
 import torch
