@@ -256,7 +256,8 @@ mp_status mp_fsep_layer_check(mp_fsep_layer* layer, uint32_t* bits);
 /* Test hook forcing a failure condition: "drop_restore_flag" (copy-engine mode:
  * the next restore skips one readiness flag -> bit 2), "barrier_timeout"
  * (virtual mode: emulated rank 0 enters a peer barrier alone -> bit 1),
- * "overwrite_guard" (one byte past the first buffer -> bit 3). */
+ * "overwrite_guard" (one byte past the first buffer -> bit 3); "clear_errors" drops
+ * the error words that have landed without reporting them (profiling probes only). */
 mp_status mp_fsep_layer_debug_inject(mp_fsep_layer* layer, const char* what);
 /* Transport probe: `iters` back-to-back full shard restores of the current layout
  * through the push transport (copy engines, or the SM push kernel with

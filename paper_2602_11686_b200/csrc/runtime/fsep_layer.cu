@@ -1627,6 +1627,8 @@ mp_status mp_fsep_layer_debug_inject(mp_fsep_layer* L, const char* what) {
     if (w == "drop_restore_flag") {
       require(L->ce_mode, "drop_restore_flag needs copy-engine mode");
       L->drop_flag = L->virt ? 1 : L->ranks[0].rank;  // virtual: emulated rank 1's push to a peer
+    } else if (w == "clear_errors") {  // drop the landed error words without reporting (profiling probes)
+      take_errors(*L);
     } else if (w == "overwrite_guard") {  // a one-byte overrun past x_rows of the first local rank
       const Guard& g = L->ranks[0].guards.front();
       CK(cudaMemset(const_cast<unsigned char*>(g.at), 0, 1));
