@@ -12,7 +12,9 @@
 //
 // Block = kBlockTokens (64) tokens x all E experts.  The hidden dimension is
 // streamed in 64-wide chunks staged (bf16 -> fp32, transposed h-major) in shared
-// memory; each thread owns a TT x TE (tokens x experts) register tile.
+// memory; each thread owns a TT x TE (tokens x experts) register tile.  Staging
+// reads whole 128-B row pieces per 8 lanes (coalesced); the transposed stores are
+// XOR-swizzled by the h octet so they stay bank-conflict free.
 #include <cuda_bf16.h>
 
 #include <cfloat>
@@ -49,8 +51,10 @@ __global__ void __launch_bounds__(512) router_gemm_kernel(const __nv_bfloat16* _
   constexpr int BT = kBlockTokens;
   constexpr int kWords = BT / 32;
   extern __shared__ float smem[];
-  float* s_x = smem;                // [kHC][BT]    h-major
-  float* s_w = smem + kHC * BT;     // [kHC][E]     h-major
+  // column c of row h lives at c ^ swz(h) (swz keeps 4-column groups aligned)
+  const int EW = (E + 31) & ~31;    // 32-aligned row stride of the weight tile
+  float* s_x = smem;                // [kHC][BT]    h-major, swizzled
+  float* s_w = smem + kHC * BT;     // [kHC][EW]    h-major, swizzled
   float* s_logit = smem;            // [BT][E + 1]  (reuses the staging area afterwards)
   __shared__ int s_idx[BT][8];
   __shared__ unsigned s_mask[kMaxExperts][kWords];
@@ -67,46 +71,60 @@ __global__ void __launch_bounds__(512) router_gemm_kernel(const __nv_bfloat16* _
 #pragma unroll
     for (int j = 0; j < TE; ++j) acc[i][j] = 0.f;
 
-  // staging work items: x = BT tokens x 8 sixteen-byte pieces; w = E x 8 pieces
+  // staging work items: x = BT tokens x 8 sixteen-byte pieces; w = E x 8 pieces.
+  // Eight consecutive items are the eight pieces of one row (one 128-B line).
   const int x_items = BT * (kHC / 8), w_items = E * (kHC / 8);
   for (int h0 = 0; h0 < H; h0 += kHC) {
     __syncthreads();
     for (int it = tid; it < x_items; it += nthr) {
-      const int tt = it % BT, piece = it / BT;
+      const int tt = it >> 3, piece = it & 7;
       const int t = min(t0 + tt, T - 1);  // clamp: rows past T are never selected
       const uint4 q = __ldg(reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * H + h0) + piece);
       const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+      const int col = tt ^ (piece << 2);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float2 f = __bfloat1622float2(b[k]);
-        s_x[(piece * 8 + 2 * k) * BT + tt] = f.x;
-        s_x[(piece * 8 + 2 * k + 1) * BT + tt] = f.y;
+        s_x[(piece * 8 + 2 * k) * BT + col] = f.x;
+        s_x[(piece * 8 + 2 * k + 1) * BT + col] = f.y;
       }
     }
     for (int it = tid; it < w_items; it += nthr) {
-      const int e = it % E, piece = it / E;
+      const int e = it >> 3, piece = it & 7;
       const uint4 q = __ldg(reinterpret_cast<const uint4*>(wg + static_cast<size_t>(e) * H + h0) + piece);
       const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+      const int col = e ^ (piece << 2);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float2 f = __bfloat1622float2(b[k]);
-        s_w[(piece * 8 + 2 * k) * E + e] = f.x;
-        s_w[(piece * 8 + 2 * k + 1) * E + e] = f.y;
+        s_w[(piece * 8 + 2 * k) * EW + col] = f.x;
+        s_w[(piece * 8 + 2 * k + 1) * EW + col] = f.y;
       }
     }
     __syncthreads();
-#pragma unroll 8
-    for (int h = 0; h < kHC; ++h) {
+    static_assert(TT % 4 == 0 && TE % 4 == 0, "register tile must be float4-aligned");
+#pragma unroll 1
+    for (int hb = 0; hb < kHC / 8; ++hb) {
+      // one h octet shares its swizzle: hoist the tile addresses, then immediate offsets
+      const int swz = hb << 2;
+      const float* xo = s_x + hb * 8 * BT;
+      const float* wo = s_w + hb * 8 * EW;
+      int xc[TT / 4], wc[TE / 4];
+#pragma unroll
+      for (int i = 0; i < TT / 4; ++i) xc[i] = (tg * TT + 4 * i) ^ swz;
+#pragma unroll
+      for (int j = 0; j < TE / 4; ++j) wc[j] = (eg * TE + 4 * j) ^ swz;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
       float xv[TT], wv[TE];
-      static_assert(TT % 4 == 0 && TE % 4 == 0, "register tile must be float4-aligned");
 #pragma unroll
       for (int i = 0; i < TT; i += 4) {
-        const float4 v = *reinterpret_cast<const float4*>(s_x + h * BT + tg * TT + i);
+        const float4 v = *reinterpret_cast<const float4*>(xo + u * BT + xc[i / 4]);
         xv[i] = v.x, xv[i + 1] = v.y, xv[i + 2] = v.z, xv[i + 3] = v.w;
       }
 #pragma unroll
       for (int j = 0; j < TE; j += 4) {
-        const float4 v = *reinterpret_cast<const float4*>(s_w + h * E + eg * TE + j);
+        const float4 v = *reinterpret_cast<const float4*>(wo + u * EW + wc[j / 4]);
         wv[j] = v.x, wv[j + 1] = v.y, wv[j + 2] = v.z, wv[j + 3] = v.w;
       }
 #pragma unroll
@@ -118,6 +136,7 @@ __global__ void __launch_bounds__(512) router_gemm_kernel(const __nv_bfloat16* _
           acc[i][j] = r.x;
           acc[i][j + 1] = r.y;
         }
+    }
     }
   }
   __syncthreads();
@@ -443,7 +462,7 @@ __global__ void __launch_bounds__(kBlockTokens * E_ / 2) router_pair_kernel(
 template <int TT, int TE>
 void launch_tiled(const RouterArgs& a, int nblk, cudaStream_t st) {
   const int threads = (kBlockTokens / TT) * (a.E / TE);
-  const size_t smem = static_cast<size_t>(kHC) * (kBlockTokens + a.E) * sizeof(float);
+  const size_t smem = static_cast<size_t>(kHC) * (kBlockTokens + ((a.E + 31) & ~31)) * sizeof(float);
   set_smem_attr(reinterpret_cast<const void*>(router_gemm_kernel<TT, TE>), 96 * 1024);
   router_gemm_kernel<TT, TE><<<nblk, threads, smem, st>>>(a.x, a.wg, a.bias, a.T, a.H, a.E, a.K, a.topk_idx,
                                                           a.topk_w, a.intra_rank, a.blk_hist);
@@ -485,7 +504,7 @@ void launch_router(const RouterArgs& a, cudaStream_t st) {
     }();
     if (tile == 8 && a.E % 8 == 0)
       launch_tiled<8, 8>(a, nblk, st);  // 8 x E/8 threads, 8x8 register tiles (half the smem traffic per FMA)
-    else if (a.E > 128)
+    else if (a.E > 128 || tile == 84)
       launch_tiled<8, 4>(a, nblk, st);  // 8 x E/4 threads (<= 512 for E <= 256)
     else
       launch_tiled<4, 4>(a, nblk, st);  // 16 x E/4 threads
