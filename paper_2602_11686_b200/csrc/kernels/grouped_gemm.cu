@@ -213,6 +213,14 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
     return v && std::string(v) == "0";
   }();
   if (no_mtail) p.policy |= 0x1000;
+  // FSEP_KSNAKE: bit k = odd waves of GemmKind k load K backwards.  Default: every kind but
+  // the gate-up GEMM (measured: -7 to -19 % DRAM reads on the other launches, Mixtral
+  // step +1.2 %, fine level; gate-up reads +2 %)
+  static const int ksnake_kinds = [] {
+    const char* v = std::getenv("FSEP_KSNAKE");
+    return v ? static_cast<int>(std::strtol(v, nullptr, 0)) : 0x1E;
+  }();
+  if ((ksnake_kinds >> static_cast<int>(kind)) & 1) p.policy |= 0x4000;
   // the gate-up GEMM's M=128 tail tiles stage B as [gate 64 | up 64] halves (64-row box map)
   const CUtensorMap& b64 = a.b64 != nullptr ? *a.b64 : tmB;
   if (kind == GemmKind::kFwdGateUp && a.b64 != nullptr) p.policy |= 0x2000;

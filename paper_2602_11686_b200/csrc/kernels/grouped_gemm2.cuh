@@ -276,7 +276,12 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
         // UMMA N=128, each CTA providing 64 columns
         const bool n_tail = p.N - nbk * BN <= HALF && !(p.policy & 0x100);
         const int n_half = nbk * BN + rank * (n_tail ? HALF / 2 : HALF);
-        for (int kb = 0; kb < nk; ++kb) {
+        // policy bit 14: odd waves stream K backwards, so they start on the k-blocks of the
+        // panels the previous wave touched last (still in L2).  Only the load order changes:
+        // the MMA accumulates in arrival order.
+        const bool krev = (p.policy & 0x4000) && (w & 1);
+        for (int kq = 0; kq < nk; ++kq) {
+          const int kb = krev ? nk - 1 - kq : kq;
           {
             FSEP_STALL_T0();
             mbar_wait(&empty_bar[s], ph ^ 1);
