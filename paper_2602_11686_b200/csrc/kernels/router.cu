@@ -62,7 +62,10 @@ __global__ void __launch_bounds__(512) router_gemm_kernel(const __nv_bfloat16* _
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int t0 = blockIdx.x * BT;
   const int egroups = E / TE;
-  const int tg = tid / egroups, eg = tid % egroups;  // this thread's tile
+  // the block is rounded up to whole warps (the top-k below shuffles over full warps);
+  // threads past the ntg x egroups tiles only stage and rank
+  const bool tiled = tid < (BT / TT) * egroups;
+  const int tg = tiled ? tid / egroups : 0, eg = tiled ? tid % egroups : 0;  // this thread's tile
   for (int i = tid; i < kMaxExperts * kWords; i += nthr) (&s_mask[0][0])[i] = 0u;
 
   float acc[TT][TE];
@@ -141,6 +144,7 @@ __global__ void __launch_bounds__(512) router_gemm_kernel(const __nv_bfloat16* _
   }
   __syncthreads();
   // logits (+ bias) -> shared memory
+  if (tiled)
 #pragma unroll
   for (int i = 0; i < TT; ++i) {
     const int tt = tg * TT + i;
@@ -461,7 +465,7 @@ __global__ void __launch_bounds__(kBlockTokens * E_ / 2) router_pair_kernel(
 
 template <int TT, int TE>
 void launch_tiled(const RouterArgs& a, int nblk, cudaStream_t st) {
-  const int threads = (kBlockTokens / TT) * (a.E / TE);
+  const int threads = ((kBlockTokens / TT) * (a.E / TE) + 31) & ~31;
   const size_t smem = static_cast<size_t>(kHC) * (kBlockTokens + ((a.E + 31) & ~31)) * sizeof(float);
   set_smem_attr(reinterpret_cast<const void*>(router_gemm_kernel<TT, TE>), 96 * 1024);
   router_gemm_kernel<TT, TE><<<nblk, threads, smem, st>>>(a.x, a.wg, a.bias, a.T, a.H, a.E, a.K, a.topk_idx,

@@ -20,7 +20,8 @@ pytestmark = pytest.mark.gpu
     (4, 256, 8, 7168, 256, 64, 64),   # DeepSeek-V3 routing and hidden size (reduced FFN and tokens)
     (2, 160, 6, 5120, 384, 96, 96),   # hidden 5120 (CH = 20), E not a power of two
     (4, 24, 2, 3072, 640, 128, 12),   # hidden 3072 (CH = 12), small E
-], ids=["e256_h7168", "e160_h5120", "e24_h3072"])
+    (2, 136, 4, 1024, 256, 100, 68),  # E > 128, not a multiple of 16: router block padded to whole warps
+], ids=["e256_h7168", "e160_h5120", "e24_h3072", "e136_padded_router"])
 def test_wide_shapes_copy_engine(N, E, K, H, F, T, C):
     g = torch.Generator(device="cuda").manual_seed(E + H)
     W = {e: ((torch.randn(F, H, device="cuda", generator=g) / H ** 0.5).bfloat16(),
