@@ -28,6 +28,7 @@
 // the device (the grouped GEMMs schedule their tiles from them).
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <array>
@@ -284,7 +285,32 @@ std::vector<int> hosted_experts(const uint8_t* A, int E, int N, int d) {
   return out;
 }
 
+// NVTX (header-only v3: no-ops unless a tool is attached): an instantaneous marker
+// at every phase boundary on the host timeline, named after the phase that ends
+// there, and ranges around the public forward / backward / graph_step calls
+// (NvtxRange below), so ncu --nvtx / nsys attribute each kernel to its stage.
+const char* phase_name(int phase) {
+  static const char* const kNames[] = {
+      "fsep:fwd_begin",      "fsep:param_barrier", "fsep:router",           "fsep:R_barrier",
+      "fsep:plan",           "fsep:dispatch",      "fsep:dispatch_barrier", "fsep:restore_wait",
+      "fsep:fwd_gemm_gateup", "fsep:fwd_gemm_down", "fsep:fwd_barrier",     "fsep:combine",
+      "fsep:combine_bwd",    "fsep:combine_bwd_barrier", "fsep:bwd_gemms",  "fsep:rs_push_wait",
+      "fsep:rs_barrier",     "fsep:bwd_barrier",   "fsep:unpermute",        "fsep:grad_rs",
+      "fsep:restore_begin",  "fsep:restore_end",   "fsep:step_begin",       "fsep:hist_d2h",
+      "fsep:planned"};
+  static_assert(sizeof(kNames) / sizeof(kNames[0]) == kPhCount + 2, "one NVTX name per phase");
+  return phase >= 0 && phase < kPhCount + 2 ? kNames[phase] : "fsep:?";
+}
+
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 void mark(mp_fsep_layer& L, cudaStream_t st, int phase) {
+  nvtxMarkA(phase_name(phase));
   if (!L.phase_on) return;
   cudaEventRecord(L.ev_p[static_cast<size_t>(L.step_no % mp_fsep_layer::kPhaseRing)][phase], st);
 }
@@ -1409,6 +1435,7 @@ mp_status mp_fsep_layer_attach_planner(mp_fsep_layer* L, mp_fsep_planner* planne
 mp_status mp_fsep_layer_forward(mp_fsep_layer* L, const void* x, const float* bias, uint32_t n_tokens, void* y,
                                 void* stream) {
   return guarded([&] {
+    const NvtxRange range("fsep.forward");
     require(L && x && y, "mp_fsep_layer_forward: NULL argument");
     require(L->connected, "mp_fsep_layer_forward: multi-GPU layer not connected");
     CK(cudaSetDevice(L->device));
@@ -1422,6 +1449,7 @@ mp_status mp_fsep_layer_forward(mp_fsep_layer* L, const void* x, const float* bi
 
 mp_status mp_fsep_layer_backward(mp_fsep_layer* L, const void* dy, void* dx, void* stream) {
   return guarded([&] {
+    const NvtxRange range("fsep.backward");
     require(L && dy && dx, "mp_fsep_layer_backward: NULL argument");
     CK(cudaSetDevice(L->device));
     poll_errors(*L);
@@ -1732,6 +1760,7 @@ mp_status mp_fsep_layer_stats_reset(mp_fsep_layer* L) {
 mp_status mp_fsep_layer_graph_step(mp_fsep_layer* L, const void* x, const float* bias, uint32_t n_tokens, void* y,
                                    const void* dy, void* dx, void* stream) {
   return guarded([&] {
+    const NvtxRange range("fsep.graph_step");
     require(L && x && y && dy && dx, "mp_fsep_layer_graph_step: NULL argument");
     auto st = static_cast<cudaStream_t>(stream);
     CK(cudaSetDevice(L->device));
