@@ -1014,7 +1014,16 @@ void raise_errors(uint32_t bits) {
   throw Error(ErrorKind::device, m);
 }
 
-void poll_errors(Layer& L) { raise_errors(take_errors(L)); }
+// Device-detected failures (host-mapped words) and, on the NCCL transport, an
+// asynchronous communicator failure (a peer gone, a network error) -> MP_ERR_DEVICE.
+void poll_errors(Layer& L) {
+  raise_errors(take_errors(L));
+  if (L.nccl != nullptr) {
+    ncclResult_t async = ncclSuccess;
+    nccl_check(ncclCommGetAsyncError(L.nccl, &async), "ncclCommGetAsyncError");
+    if (async != ncclSuccess && async != ncclInProgress) nccl_check(async, "NCCL communicator failed asynchronously");
+  }
+}
 
 bool is_device_ptr(const void* p) {
   cudaPointerAttributes a{};
