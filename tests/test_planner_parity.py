@@ -183,3 +183,28 @@ def test_plan_next_matches_planner_handle_and_port(product_lib):
         want = PORT.plan_layout([R.astype(np.int64).tolist()], topo, params, c,
                                 PORT.SearchSpec(4, PORT.mix_seed(5, 0x6C617972, layer)))
         assert np.array_equal(A, np.array(want, dtype=np.uint8))
+
+
+@pytest.mark.parametrize("nodes,dpn,e,c", [(8, 8, 128, 2), (16, 8, 256, 4), (4, 8, 64, 8), (1, 72, 256, 4), (128, 8, 1024, 2)])
+def test_large_instances_byte_identical(product_lib, ref, tmp_path, nodes, dpn, e, c):
+    """Cluster-scale instances (64-1024 devices, up to 1024 experts; the relocation's node
+    balancing and repair paths get exercised far more than at <= 12 devices)."""
+    n = nodes * dpn
+    rng = np.random.default_rng(n * 1000 + e + c)
+    cfg = json.dumps({
+        "topology": {"n_nodes": nodes, "devices_per_node": dpn, "b_intra": 9e11, "b_inter": 5e10},
+        "cost": {"v_comm": 8192.0, "v_comp": 3.52e8, "b_comp": 1.6354e15, "f_ckpt": 0},
+        "model": {"n_experts": e, "capacity": c},
+        "planner": {"epsilon": 3, "seed": int(rng.integers(1 << 62)), "history": "ema", "ema_decay": 0.5},
+    })
+    lines = []
+    for t in range(3):
+        p = rng.permutation(e)
+        w = (np.arange(1, e + 1, dtype=np.float64) ** -1.2)[p]
+        R = np.stack([rng.multinomial(4096 * 8, w / w.sum()) for _ in range(n)])
+        lines.append(json.dumps({"iter": t, "layer": 0, "R": R.astype(int).tolist()}))
+    path = tmp_path / "large.jsonl"
+    path.write_text("\n".join(lines) + "\n")
+    mine = PP.plan_layer_json(PP.Config(cfg), PP.Trace.load(str(path)), 0)
+    theirs = ref.plan_layer_json(ref.config(cfg), ref.trace_load(str(path)), 0)
+    assert mine == theirs
