@@ -1,7 +1,7 @@
-"""Seeded random layer shapes on emulated ranks vs the oracle: world sizes 1-8 (incl. 3 and
-5), top-k 1-8, ragged token counts (not multiples of the 64-token router tile), hidden
-sizes from the supported set, capacities from the minimum (E/N) to full replication,
-planned or static layouts, and both transports (device kernels / the shipped copy-engine
+"""Seeded random layer shapes on emulated ranks vs the oracle: world sizes 1-8 (incl. 3,
+5 and 6) plus the 16-rank maximum, top-k 1-8, ragged token counts (not multiples of the
+64-token router tile), hidden sizes from the supported set, capacities from the minimum
+(E/N) to full replication, planned or static layouts, and both transports (device kernels / the shipped copy-engine
 path).  Routing bit-exact; y, dx, router and expert gradients within 2e-2."""
 import random
 
@@ -36,7 +36,11 @@ def _cases(n):
     return out
 
 
-@pytest.mark.parametrize("N,E,K,H,F,T,C,layout,ce", _cases(16))
+# plus the largest world the runtime supports (16 ranks) on both transports
+_EXTRA = [(16, 32, 4, 256, 128, 64, 2, "planned", True), (16, 48, 6, 512, 256, 33, 4, "static", False)]
+
+
+@pytest.mark.parametrize("N,E,K,H,F,T,C,layout,ce", _cases(16) + _EXTRA)
 def test_random_shape(N, E, K, H, F, T, C, layout, ce):
     pb = make_problem(N, E, K, H, F, T, 1.1, seed=N * 1000 + E * 10 + K)
     if layout == "static":
