@@ -163,15 +163,20 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
   // long-K M-grouped GEMMs only: their A / B panels (256 x K) do not stay in L2 when the
   // CTA pairs drift apart along K (Mixtral up-dgrad, K = 28672: DRAM reads 11.9 -> 9.7 GB,
   // step +2.5-5%); short-K panels fit in L2 anyway and the barrier only costs (fine config)
-  // K-grouped wgrad: only when every group spans several waves (equal-cost tiles within a
-  // wave; a wave that mixes groups of different row counts would idle at the barrier)
-  static const bool wave_sync_wgrad = [] {  // FSEP_WAVE_SYNC_WGRAD=0: wgrad producers free-running
+  // K-grouped wgrad: every launch.  A wave that mixes groups of different row counts idles
+  // at the barrier (LPT order keeps neighbours similar), but free-running pairs drift apart
+  // along the hot experts' long K and re-read their panels: fine dW13 DRAM reads 10.9 ->
+  // 3.6 GB, fine step +0.6 to +3.5 % at N=1 and +1.7 % at N=4 (profiles/r02/wgrad_sync/).
+  // FSEP_WAVE_SYNC_WGRAD=0: free-running; =big: only groups spanning >= 2 waves (round 1)
+  static const int wave_sync_wgrad = [] {
     const char* v = std::getenv("FSEP_WAVE_SYNC_WGRAD");
-    return !(v && std::string(v) == "0");
+    return !v ? 2 : std::string(v) == "0" ? 0 : std::string(v) == "big" ? 1 : 2;
   }();
-  const bool long_k = kind == GemmKind::kBwdWgrad
-                          ? wave_sync_wgrad && (a.M / gemm2::BM) * ((a.N + gemm2::BN - 1) / gemm2::BN) >= 2 * num_sms
-                          : a.K >= 4096;
+  const bool long_k =
+      kind == GemmKind::kBwdWgrad
+          ? wave_sync_wgrad == 2 ||
+                (wave_sync_wgrad == 1 && (a.M / gemm2::BM) * ((a.N + gemm2::BN - 1) / gemm2::BN) >= 2 * num_sms)
+          : a.K >= 4096;
   // FSEP_WGRAD_RASTER: tile order of the wgrad launches (A/B; see GemmParams::raster).  n-inner
   // for the Mixtral dW13 (112 x 16 tiles) halves its DRAM reads (10.8 -> 5.8 GB) but measured
   // ~1% slower over the step, so the default stays 16-tile m-chunks.
