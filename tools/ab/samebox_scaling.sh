@@ -1,5 +1,5 @@
 # weak scaling on one 4-GPU box: N=1 (GPU 0), N=2, N=4, Mixtral and fine, alternated twice
-o=gpurun_out/r02sc; mkdir -p $o
+o=${O:-gpurun_out/r02sc}; mkdir -p $o
 for rep in 1 2; do
   for cfg in mixtral fine; do
     CUDA_VISIBLE_DEVICES=0 python bench.py --config $cfg --steps 10 --warmup 3 --no-e2e --no-cpu > $o/${cfg}_n1_$rep.json 2>/dev/null
