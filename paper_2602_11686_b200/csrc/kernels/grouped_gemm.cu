@@ -177,14 +177,21 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
           ? wave_sync_wgrad == 2 ||
                 (wave_sync_wgrad == 1 && (a.M / gemm2::BM) * ((a.N + gemm2::BN - 1) / gemm2::BN) >= 2 * num_sms)
           : a.K >= 4096;
-  // FSEP_WGRAD_RASTER: tile order of the wgrad launches (A/B; see GemmParams::raster).  n-inner
-  // for the Mixtral dW13 (112 x 16 tiles) halves its DRAM reads (10.8 -> 5.8 GB) but measured
-  // ~1% slower over the step, so the default stays 16-tile m-chunks.
+  // Tile order of the wgrad launches: for groups spanning several waves, the panels along
+  // the shorter tile dimension stay resident in L2 for the whole group while the other side
+  // streams past them once -- n fastest when a group has no more n tiles than m tiles
+  // (Mixtral dW13, 112 x 16: DRAM reads 6.3 -> 4.4 GB, step +0.5 %), else 16-tile m-chunks
+  // (dW2, 16 x 56: n-fastest there would re-read 8 GB; small groups, e.g. the fine
+  // config's 11 x 8, measured level-to-worse with n-fastest).  FSEP_WGRAD_RASTER overrides.
   static const int wgrad_raster = [] {
     const char* v = std::getenv("FSEP_WGRAD_RASTER");
-    return v ? std::atoi(v) : 0;
+    return v ? std::atoi(v) : -1;
   }();
-  if (kind == GemmKind::kBwdWgrad && p.raster == 0) p.raster = wgrad_raster;
+  if (kind == GemmKind::kBwdWgrad && p.raster == 0) {
+    const int m_tiles = a.M / gemm2::BM, n_tiles = (a.N + gemm2::BN - 1) / gemm2::BN;
+    const bool big = m_tiles * n_tiles >= 2 * num_sms;
+    p.raster = wgrad_raster >= 0 ? wgrad_raster : (big && n_tiles <= m_tiles ? 2 : 0);
+  }
   // FSEP_MRASTER[_<kind>]: m-chunk of the M-grouped launches' tile order (A/B; default 16 m tiles,
   // n-inner: an A chunk of 16 x 256 rows stays in L2 while the B panels stream past it)
   static const int mraster[4] = {env_raster(0), env_raster(1), env_raster(2), env_raster(3)};
