@@ -168,6 +168,10 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
   // along the hot experts' long K and re-read their panels: fine dW13 DRAM reads 10.9 ->
   // 3.6 GB, fine step +0.6 to +3.5 % at N=1 and +1.7 % at N=4 (profiles/r02/wgrad_sync/).
   // FSEP_WAVE_SYNC_WGRAD=0: free-running; =big: only groups spanning >= 2 waves (round 1)
+  static const int wave_sync_min_k = [] {  // FSEP_WAVE_SYNC_MIN_K: shortest K synchronised (A/B)
+    const char* v = std::getenv("FSEP_WAVE_SYNC_MIN_K");
+    return v ? std::atoi(v) : 4096;
+  }();
   static const int wave_sync_wgrad = [] {
     const char* v = std::getenv("FSEP_WAVE_SYNC_WGRAD");
     return !v ? 2 : std::string(v) == "0" ? 0 : std::string(v) == "big" ? 1 : 2;
@@ -176,7 +180,7 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
       kind == GemmKind::kBwdWgrad
           ? wave_sync_wgrad == 2 ||
                 (wave_sync_wgrad == 1 && (a.M / gemm2::BM) * ((a.N + gemm2::BN - 1) / gemm2::BN) >= 2 * num_sms)
-          : a.K >= 4096;
+          : a.K >= wave_sync_min_k;
   // Tile order of the wgrad launches: for groups spanning several waves, the panels along
   // the shorter tile dimension stay resident in L2 for the whole group while the other side
   // streams past them once -- n fastest when a group has no more n tiles than m tiles
