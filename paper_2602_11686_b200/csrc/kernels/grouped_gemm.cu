@@ -237,6 +237,11 @@ void launch_grouped_gemm_pair(GemmKind kind, const CUtensorMap& tmA, const CUten
     return v ? static_cast<int>(std::strtol(v, nullptr, 0)) : 0x1E;
   }();
   if ((ksnake_kinds >> static_cast<int>(kind)) & 1) p.policy |= 0x4000;
+  static const bool no_h_prefetch = [] {  // FSEP_H_PREFETCH=0: no L2 prefetch of h in the SwiGLU' epilogue (A/B)
+    const char* v = std::getenv("FSEP_H_PREFETCH");
+    return v && std::string(v) == "0";
+  }();
+  if (no_h_prefetch) p.policy |= 0x8000;
   // the gate-up GEMM's M=128 tail tiles stage B as [gate 64 | up 64] halves (64-row box map)
   const CUtensorMap& b64 = a.b64 != nullptr ? *a.b64 : tmB;
   if (kind == GemmKind::kFwdGateUp && a.b64 != nullptr) p.policy |= 0x2000;

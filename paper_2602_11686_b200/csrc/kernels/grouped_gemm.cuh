@@ -55,6 +55,7 @@ struct GemmParams {
                // bit 12: no M=128 tail tiles (masked M=256 tiles instead; A/B)
                // bit 13: the launch has a 64-row-box B map (gate-up M=128 tail tiles)
                // bit 14: odd waves load their k-blocks in reverse order (L2 reuse across waves; A/B)
+               // bit 15: no L2 prefetch of h in the SwiGLU' epilogue (A/B)
   int raster;  // tile order within a group: 0 mode default, 1 m-inner, 2 n-inner, 3+ = m-chunks of `raster` tiles, n-inner
   // Optional per-group readiness (M-grouped only): before loading B of group g the
   // producer waits until ready[g * ready_n + q] has reached ready_epoch for all

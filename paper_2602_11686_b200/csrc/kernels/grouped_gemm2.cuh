@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
                            : m_half + static_cast<int>(quarter) * 32;
       const int tcw = mt ? tn / 4 : HALF;
       const bool valid = kGroupK || mt || m_half < p.group_rows[g];
-      if (kEpi == kEpiSwigluBwd && valid && !mt) {
+      if (kEpi == kEpiSwigluBwd && valid && !mt && !(p.policy & 0x8000)) {
         // While the MMAs of this tile run, pull this row's h slice (one 128-feature
         // block: 256 contiguous bf16 = 512 B) into L2 so the epilogue loads hit L2.
         for (int half = half0; half < half0 + NHALF; ++half) {
