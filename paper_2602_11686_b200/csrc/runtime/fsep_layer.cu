@@ -184,7 +184,7 @@ extern "C" struct mp_fsep_layer {
   // reduce-scatter gathers run as peer cudaMemcpyAsync on one stream per peer,
   // using no SMs; the forward GEMMs poll per-(slot, peer) readiness flags.
   bool ce_mode = false;
-  // copy-engine lanes: ce_k streams per destination rank (FSEP_CE_STREAMS), lane d*ce_k + j;
+  // copy-engine lanes: ce_k streams per destination rank (1 or 2 by chunk size; FSEP_CE_STREAMS), lane d*ce_k + j;
   // slot / chunk c of destination d travels on lane d*ce_k + c % ce_k
   static constexpr int kMaxLanes = 4;
   int ce_k = 1;
@@ -1109,6 +1109,12 @@ mp_status mp_fsep_layer_create(const mp_fsep_desc* desc, int device, mp_fsep_lay
     // flags.  A second kernel launched after dispatch could not always get CTAs beside the
     // GEMM (flags then only landed after the readiness timeout) -- measured, Mixtral N=8.
     if (L->sm_push && !std::getenv("FSEP_RESTORE_SPLIT")) L->restore_split = false;
+    // Two copy-engine lanes per peer when each restored chunk is large (Mixtral: 88 MB at
+    // N=4; tokens/s +0.3 % at T=16384, +0.1 % at T=4096 over 3 alternations,
+    // profiles/r02/ce_auto_lanes/); one for small chunks, where a second lane only adds
+    // contention with the GEMMs (fine config, 4.3 MB chunks: -1.9 % / -3.3 %,
+    // profiles/r02/n4_ce_lanes_*).
+    L->ce_k = L->S * 2 >= (32ll << 20) ? 2 : 1;
     if (const char* v = std::getenv("FSEP_CE_STREAMS")) L->ce_k = std::clamp(std::atoi(v), 1, mp_fsep_layer::kMaxLanes);
     if (const char* v = std::getenv("FSEP_PUSH_CTAS")) L->push_ctas = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("FSEP_PUSH_PIECE_KB"))
