@@ -127,6 +127,49 @@ def test_planner_steps_copy_engine(transport):
     layer.close()
 
 
+def test_soak_200_steps_drifting_copy_engine(transport):
+    """200 steps with the planner attached and the routing skew re-drawn every step:
+    200 restore epochs of readiness flags and reduce-scatter pushes.  Every step: no
+    device-detected failure and the layout the host planner predicts; steps 0, 99 and
+    199 in full vs the oracle."""
+    N, E, K, H, F, T, C = 4, 8, 2, 256, 256, 128, 3
+    layer = FsepLayer(LayerSpec(E, K, H, F, T, C, world=N, virtual=True, copy_engine=True))
+    pb = make_problem(N, E, K, H, F, T, 1.2, seed=21)
+    for e in range(E):
+        layer.load_expert(e, pb["w1"][e].cuda().contiguous(), pb["w3"][e].cuda().contiguous(),
+                          pb["w2"][e].cuda().contiguous())
+    layer.load_router(pb["wg"].cuda())
+    cfg = PL.Config(json.dumps({"topology": {"n_nodes": 1, "devices_per_node": N, "b_intra": 9e11, "b_inter": 9e11},
+                                "cost": {"v_comm": 2 * H, "v_comp": 6 * H * F, "b_comp": 1.6354e15},
+                                "model": {"n_experts": E, "capacity": C}, "planner": {"seed": 3}}))
+    layer.attach_planner(cfg, layer=0)
+    x = torch.cat(pb["xs"]).cuda()
+    dy = torch.cat(pb["dys"]).cuda()
+    y, dx = torch.empty_like(x), torch.empty_like(x)
+    topo = PP.Topology(1, N, 9e11, 9e11)
+    params = PP.CostParams(2 * H, 6 * H * F, 1.6354e15)
+    history, changes = [], 0
+    A = np.array(PP.even_replication_layout(topo, E, C), dtype=np.uint8)
+    for step in range(200):
+        rng = np.random.default_rng(1000 + step)
+        biases = [LO.make_bias(rng, T, E, 0.6 + 0.9 * rng.random(), rng.permutation(E)) for _ in range(N)]
+        layer.forward(x, torch.from_numpy(np.concatenate(biases)).cuda(), T, y)
+        layer.backward(dy, dx)
+        assert layer.check() == 0, step
+        assert np.array_equal(layer.read("layout", 0).reshape(E, N), A), step
+        if step in (0, 99, 199):
+            ref = oracle(dict(pb, biases=biases), K, A, C)
+            check_routing(layer, ref, N, T, K, C)
+            check_numerics(layer, ref, y, dx, N, T, H, E)
+        history.append(layer.histogram().astype(np.int64).tolist())
+        nxt = np.array(PP.plan_layout(history, topo, params, C, PP.SearchSpec(2, PP.mix_seed(3, 0x6C617972, 0))),
+                       dtype=np.uint8)
+        changes += int(not np.array_equal(nxt, A))
+        A = nxt
+    assert changes >= 10, f"the planner changed the layout only {changes} times"
+    layer.close()
+
+
 def _mixtral_n8_run(copy_engine, w, xs, dys, biases, A, E, K, H, F, T, C, N):
     layer = FsepLayer(LayerSpec(E, K, H, F, T, C, world=N, virtual=True, copy_engine=copy_engine))
     for e in range(E):
