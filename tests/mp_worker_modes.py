@@ -14,6 +14,8 @@ one process per GPU, copy-engine communication).  Checks, in real multi-GPU mode
 * the SM push transport (FSEP_COMM=sm) and the NCCL transport (FSEP_COMM=nccl:
   grouped ncclSend/ncclRecv restore and gradient exchange) are bit-identical to the
   copy engines;
+* a 100-step soak with the planner attached and the routing skew re-drawn every step
+  (healthy every 10th step; the last step vs the oracle on the layout it used);
 * no device-detected failure (barrier / readiness timeouts, overflow, memory guards).
 Exits non-zero on the first mismatch."""
 import json
@@ -163,6 +165,33 @@ def main():
     assert np.array_equal(code & 0xFFFFFF, ref["routing"].slot_row[rank]), "local-first slot rows differ"
     err = float(np.abs(y.cpu().float().numpy() - ref["y"][rank]).max() / np.abs(ref["y"][rank]).max())
     assert err < 2e-2, f"local-first y rel err {err}"
+    layer.close()
+
+    # 4. soak: 100 steps, planner attached, routing skew re-drawn every step -- every 10th
+    # step healthy, and the last step vs the oracle on the layout the layer used
+    C = E // world + 1  # one spare slot per device: the planner has replicas to move
+    W = weights(41)
+    layer = make_layer(world, rank, C, W)
+    layer.attach_planner(config(world, C), layer=0)
+    y = torch.empty_like(x_d)
+    dx = torch.empty_like(x_d)
+    for step in range(100):
+        rng = np.random.default_rng(7000 + 31 * step + rank)
+        bias = LO.make_bias(rng, T, E, 0.6 + 0.9 * np.random.default_rng(step).random(),
+                            np.random.default_rng(step).permutation(E))
+        layer.forward(x_d, torch.from_numpy(bias).cuda(), T, y)
+        layer.backward(dy_d, dx)
+        if step % 10 == 9:
+            assert layer.check() == 0, f"soak step {step}: device-detected failure"
+    torch.cuda.synchronize()
+    A = layer.read("layout").reshape(E, world)
+    allb = [None] * world
+    dist.all_gather_object(allb, bias)
+    wg, w1, w3, w2 = (t.float().numpy() for t in W)
+    ref = LO.layer_step([v[0] for v in allx], allb, wg, w1, w3, w2, K, A, C, [v[1] for v in allx])
+    for name, got, want in (("y", y, ref["y"][rank]), ("dx", dx, ref["dx"][rank])):
+        err = float(np.abs(got.cpu().float().numpy() - want).max() / max(np.abs(want).max(), 1e-30))
+        assert err < 2e-2, f"soak {name} rel err {err}"
     layer.close()
     dist.barrier()
     dist.destroy_process_group()
