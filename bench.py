@@ -239,7 +239,7 @@ def run_reference_impl(args, cfg):
 
 
 # ---------------------------------------------------------------- GPU path
-def token_kernel_bandwidth(phases, layer, PL, N, rank, T, K, H, F=0, C=0):
+def token_kernel_bandwidth(phases, layer, PL, N, rank, T, K, H, F=0, C=0, config=None):
     """HBM and NVLink throughput of the token-movement kernels (rank 0's layer 0).
 
     Algorithmic bytes per step (bf16 rows of H elements, T tokens, K slots each):
@@ -276,6 +276,20 @@ def token_kernel_bandwidth(phases, layer, PL, N, rank, T, K, H, F=0, C=0):
     hbm = peaks()[2]
     for v in out.values():
         v["hbm_frac"] = round(v["GBps"] / hbm, 4)
+    # the same kernels timed alone (committed ncu launch list of this config at N=1): in the
+    # step they run at the power-capped SM clock right after the GEMMs
+    if N == 1 and config:
+        launches = ROOT / "profiles" / "r02" / f"launches_n1_{config}_final2.txt"
+        kern = {"dispatch": "dispatch_tma_kernel", "combine": "combine_kernel<", "unpermute": "unpermute_bwd_kernel"}
+        if launches.exists():
+            for line in launches.read_text().splitlines():
+                parts = [p_.strip() for p_ in line.split("|")]
+                for name, key in kern.items():
+                    if name in out and len(parts) == 5 and key in parts[0] and not line.startswith("#"):
+                        iso = float(parts[3])
+                        out[name]["isolated_ms"] = iso
+                        out[name]["isolated_hbm_frac"] = round(out[name]["bytes"] / (iso * 1e-3) / 1e9 / hbm, 4)
+                        out[name]["isolated_source"] = str(launches.relative_to(ROOT))
     rms = phases.get("restore_landed_ms") or phases.get("restore_ms") or 0.0
     if N > 1 and F and C and rms > 0:
         b = C * 3 * H * F * 2 * (N - 1) // N
@@ -480,7 +494,7 @@ def main():
     phases = layers[0].phase_ms() if os.environ.get("FSEP_PHASE_TIMING") == "1" else None
     if phases:
         phases["fwd_gemms"] = round(phases["fwd_gemm_gateup"] + phases["fwd_gemm_down"], 4)
-    comm = token_kernel_bandwidth(phases, layers[0], PL, N, rank, T, K, H, F, C) if phases else None
+    comm = token_kernel_bandwidth(phases, layers[0], PL, N, rank, T, K, H, F, C, config=args.config) if phases else None
     per_rank = None
     if world > 1 and phases:
         # per-rank view of the phases that expose load imbalance (barrier waits absorb it)
