@@ -3,8 +3,9 @@
 # (/root/reference/proj/src, C++20) into oracle/_ref/ so the parity tests and
 # bench.py's reference arm can call the reference itself through its own C ABI
 # (moeplan.h).  Nothing is copied from the reference tree: the sources are
-# compiled where they lie.  Outputs: oracle/_ref/libmoeplan_ref.so and
-# oracle/_ref/refplan_bench (timing driver for the CPU baseline).
+# compiled where they lie.  Outputs: oracle/_ref/libmoeplan_ref.so,
+# oracle/_ref/refplan_bench (timing driver for the CPU baseline) and
+# oracle/_ref/planner_hash_ref (the reference side of the 20k-instance hash test).
 #
 # The only third-party dependency of the reference on this path is
 # nlohmann::json (vendor/json.hpp, absent from the reference tree); the image
@@ -34,4 +35,5 @@ done
 wait
 g++ -shared -Wl,-Bsymbolic -o "$OUT/libmoeplan_ref.so" "${objs[@]}"
 g++ $CXXFLAGS "$HERE/refplan_bench.cpp" "${objs[@]}" -o "$OUT/refplan_bench"
+g++ $CXXFLAGS "$HERE/planner_hash.cpp" "${objs[@]}" -o "$OUT/planner_hash_ref"
 echo "built $OUT/libmoeplan_ref.so"

@@ -208,3 +208,25 @@ def test_large_instances_byte_identical(product_lib, ref, tmp_path, nodes, dpn, 
     mine = PP.plan_layer_json(PP.Config(cfg), PP.Trace.load(str(path)), 0)
     theirs = ref.plan_layer_json(ref.config(cfg), ref.trace_load(str(path)), 0)
     assert mine == theirs
+
+
+def test_20k_instance_hash_matches_reference(product_lib):
+    """oracle/planner_hash.cpp, one source written against the shared
+    C++ API, built against the reference objects (oracle/build_ref.sh) and against this
+    library; plan_layout + lite_routing + time_cost over 20,000 seeded random instances
+    (1-32 devices, 1-4 nodes, up to 64 experts, 1-3 history steps, last / EMA, epsilon
+    2-5) must hash identically."""
+    import subprocess
+    root = Path(__file__).resolve().parents[1]
+    ref_bin = root / "oracle" / "_ref" / "planner_hash_ref"
+    if not ref_bin.exists():
+        pytest.skip("reference planner_hash not built (reference tree absent)")
+    src = root / "oracle" / "planner_hash.cpp"
+    lib = root / "paper_2602_11686_b200" / "lib"
+    ours = root / "oracle" / "_ref" / "planner_hash_b200"
+    if not ours.exists() or ours.stat().st_mtime < max(src.stat().st_mtime, (lib / "libmoeplan_b200.so").stat().st_mtime):
+        subprocess.run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", f"-I{root / 'include'}", str(src),
+                        f"-L{lib}", "-l:libmoeplan_b200.so", f"-Wl,-rpath,{lib}", "-o", str(ours)], check=True)
+    a = subprocess.run([str(ref_bin), "20000", "1"], capture_output=True, text=True, check=True).stdout.split()
+    b = subprocess.run([str(ours), "20000", "1"], capture_output=True, text=True, check=True).stdout.split()
+    assert a[0] == "20000" and a == b, (a, b)
