@@ -1,5 +1,5 @@
 # end-of-round multi-GPU lines with the final code: N=2 and N=4 full bench lines (Mixtral, fine), multilayer at N=4
-o=gpurun_out/r02fm; mkdir -p $o
+o=${O:-gpurun_out/r02fm}; mkdir -p $o
 for n in 2 4; do
   R="python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2956$n"
   timeout 1200 $R bench.py --gpus $n --steps 10 --warmup 3 > $o/mix_n$n.json 2> $o/mix_n$n.err; echo mix $n=$?
