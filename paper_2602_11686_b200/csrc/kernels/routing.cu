@@ -744,7 +744,11 @@ void launch_dispatch(const DispatchArgs& a, cudaStream_t st) {
     FSEP_CH_SWITCH(a.H / 256, {
       constexpr size_t smem = dispatch_smem<CH>() + kDispatchWarps * dispatch_bufs<CH>() * 8;
       set_smem_attr(reinterpret_cast<const void*>(dispatch_tma_kernel<CH>), static_cast<int>(smem));
-      const int blocks = std::min(sms, (a.T + kDispatchWarps - 1) / kDispatchWarps);
+      static const int per_sm = [] {  // FSEP_DISPATCH_CTAS_PER_SM: resident dispatch CTAs per SM (A/B)
+        const char* v = std::getenv("FSEP_DISPATCH_CTAS_PER_SM");
+        return v ? std::max(1, std::atoi(v)) : 1;
+      }();
+      const int blocks = std::min(sms * per_sm, (a.T + kDispatchWarps - 1) / kDispatchWarps);
       dispatch_tma_kernel<CH><<<blocks, kDispatchWarps * 32, smem, st>>>(
           a.x, a.T, a.K, a.E, a.topk_idx, a.intra_rank, a.blk_base, a.pt, a.peers, a.slot_dst, a.rank, a.topk_w,
           a.T_max, a.dedupe);
