@@ -279,7 +279,7 @@ def token_kernel_bandwidth(phases, layer, PL, N, rank, T, K, H, F=0, C=0, config
     # the same kernels timed alone (committed ncu launch list of this config at N=1): in the
     # step they run at the power-capped SM clock right after the GEMMs
     if N == 1 and config:
-        launches = ROOT / "profiles" / "r02" / f"launches_n1_{config}_final2.txt"
+        launches = ROOT / "profiles" / "r02" / f"launches_n1_{config}_final3.txt"
         kern = {"dispatch": "dispatch_tma_kernel", "combine": "combine_kernel<", "unpermute": "unpermute_bwd_kernel"}
         if launches.exists():
             for line in launches.read_text().splitlines():

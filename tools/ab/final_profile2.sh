@@ -1,6 +1,6 @@
 # profile set for the final kernels (K-snake, router staging): ncu launch lists and one-step ncu --set full captures, summarised ON THE BOX
 # captures summarised ON THE BOX (the .ncu-rep files exceed gpurun's 64 MiB copy-back limit)
-o=gpurun_out/r02f2; mkdir -p $o
+o=${O:-gpurun_out/r02f2}; mkdir -p $o
 for c in mixtral fine; do
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $o/launches_$c.csv python bench.py --config $c --steps 2 --warmup 3 --no-e2e --no-cpu > $o/ncul_$c.log 2>&1; echo ncul $c=$?
   python tools/launch_summary.py $o/launches_$c.csv $o/launches_$c.txt "ncu --metrics gpu__time_duration.sum --clock-control none: bench.py --config $c --steps 2 --warmup 3 (5 steps; cold-cache serialised launches)" 5 > /dev/null
