@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(gemm2::THREADS, 1)
   auto k_blocks = [&](int g) { return kGroupK ? p.group_rows[g] / BK : p.K / BK; };
   // M=128 tail tile: the group's last 256-row tile holds only 128 (padded) rows.  The
   // gate-up GEMM needs the 64-row-box B map for its [gate|up] halves (policy bit 13).
-  const bool tails_ok = !kGroupK && EPI_WARPS == 8 && !(p.policy & 0x1000) &&
+  const bool tails_ok = !kGroupK && !(p.policy & 0x1000) &&
                         (kEpi != kEpiSwigluFwd || (p.policy & 0x2000));
   auto m_tail = [&](int g, int mb) { return tails_ok && p.group_rows[g] - mb * BM <= HALF; };
   // Tile of this CTA pair in wave w.  K-grouped: snake order (even waves ascending,
